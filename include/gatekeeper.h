@@ -1,0 +1,160 @@
+/* gatekeeper.h -- C ABI of the B200-native GateKeeper-GPU pre-alignment filter.
+ *
+ * Method: Bingol et al., "GateKeeper-GPU: Fast and Accurate Pre-Alignment
+ * Filtering in Short Read Mapping", arXiv 2103.14978.  For every
+ * (read, candidate reference segment) pair of equal length L and an edit
+ * threshold e the filter (Fig. S.1 :444-490):
+ *   1. 2-bit encodes both sequences (A=00 C=01 G=10 T=11, :49);
+ *   2. passes pairs containing a non-ACGT byte unfiltered (:95);
+ *   3. builds the Hamming mask, amends it and counts its errors; a count <= e
+ *      accepts immediately (Fig. S.1 "e > E, therefore ASM begins", :466);
+ *   4. otherwise builds 2e shifted masks (read shifted k = 1..e bases toward
+ *      higher / lower positions), amends every mask (turns bounded 0-runs of
+ *      length <= 2 into 1s, :51), forces the vacated leading / trailing bits
+ *      to 1 (GateKeeper-GPU's edge fix, :109), ANDs all 2e+1 masks (:51);
+ *   5. counts errors in 4-base windows (runs of 1s per window, :51) and
+ *      rejects iff the count exceeds e (:51); reports the count (:166).
+ * The exact readings of the passages the paper leaves open are listed in
+ * DESIGN.md ("Readings of the paper", R1-R13).
+ *
+ * Conventions (all entry points):
+ *  - Every pointer named d_* is a DEVICE pointer (e.g. torch.Tensor.data_ptr()
+ *    of a CUDA tensor); h_* is a HOST pointer.  The caller owns every buffer;
+ *    the library never allocates, frees or retains a pointer past the call.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Device calls are asynchronous and ordered on `stream`.
+ *  - Arguments are validated on the host before any launch.  Return value:
+ *    GK_OK (0) or a negative gk_status.  A launch failure returns GK_ERR_CUDA;
+ *    gk_last_cuda_error() then gives the cudaError_t (thread-local).
+ *  - n = 0 is a valid no-op.  1 <= len <= GK_MAX_LEN; 0 <= e < len.
+ *  - No global mutable state; calls from several host threads are safe.
+ *
+ * Packed sequence layout ("bit-sliced tiles", written by gk_encode, read by
+ * gk_filter).  Sequences are grouped by 32 ("group") and groups by 32
+ * ("tile" = 1024 sequences).  Sequence s lives in tile t = s/1024, lane
+ * g = (s/32)%32, bit j = s%32.  For base i (0 <= i < len) the two 32-bit words
+ *     d_packed[((t*len + i)*32 + g)*2 + 0]   plane 0 = high bit of the code
+ *     d_packed[((t*len + i)*32 + g)*2 + 1]   plane 1 = low  bit of the code
+ * hold, at bit j, that bit of sequence s's base i.  So one 32-bit word carries
+ * one base position of 32 sequences, and a warp reading position i of a tile
+ * reads 256 contiguous bytes.  Total size: gk_packed_words(n, len) words
+ * (= ceil(n/1024)*len*64, i.e. len/4 bytes per sequence).  Sequences
+ * s >= n in the last tile are encoded as all-'A' and defined.
+ * d_undef[t*32 + g] bit j = 1 iff sequence s contains a byte outside
+ * {A,C,G,T,a,c,g,t} ("undefined"); the plane bits of an
+ * undefined sequence are unspecified.
+ *
+ * Result layout.  d_accept_bits[p/32] bit p%32 = 1 iff pair p is accepted
+ * ("1" = accept, "0" = reject); gk_result_words(n) words, bits of
+ * pairs >= n in the last word are 0.  d_errcount[p] (optional, may be NULL) =
+ * the approximate edit distance the deciding stage counted (0..254), or 255 for
+ * an undefined pair.
+ */
+#ifndef GATEKEEPER_H
+#define GATEKEEPER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GK_MAX_LEN 508      /* max count 2*ceil(508/4) = 254 fits a byte; 255 = undefined */
+#define GK_MAX_STRIDE 1024  /* row stride limit of the ASCII entry points */
+#define GK_TILE 1024        /* sequences per packed tile */
+
+typedef enum gk_status {
+  GK_OK = 0,
+  GK_ERR_ARG = -1,       /* NULL pointer where one is required, n < 0, stride < len, ... */
+  GK_ERR_LEN = -2,       /* len outside [1, GK_MAX_LEN] */
+  GK_ERR_E = -3,         /* e outside [0, len) */
+  GK_ERR_ALIGN = -4,     /* packed / result buffer not 4-byte (words) or 16-byte aligned */
+  GK_ERR_WORKSPACE = -5, /* workspace NULL or smaller than the *_workspace_bytes() query */
+  GK_ERR_CUDA = -6       /* a CUDA call failed; see gk_last_cuda_error() */
+} gk_status;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int gk_version(void);
+/* Static, NUL-terminated description of a status code. */
+const char* gk_status_string(int status);
+/* cudaError_t of the last GK_ERR_CUDA returned on this host thread (0 if none). */
+int gk_last_cuda_error(void);
+
+/* Size queries (pure host functions, no CUDA). */
+size_t gk_packed_words(int64_t n_seqs, int32_t len); /* u32 words of a packed sequence set */
+size_t gk_undef_words(int64_t n_seqs);               /* u32 words of its undefined flags */
+size_t gk_result_words(int64_t n_pairs);             /* u32 words of accept bits */
+
+/* a1: ASCII -> packed bit-sliced tiles (device encoding :105).
+ *  d_seqs   : n_seqs rows of `stride` bytes, base i of row s at d_seqs[s*stride+i];
+ *             only the first len bytes of a row are read.  len <= stride <= GK_MAX_STRIDE.
+ *  d_packed : gk_packed_words(n_seqs, len) u32, 16-byte aligned (written).
+ *  d_undef  : gk_undef_words(n_seqs) u32, 4-byte aligned (written).
+ * Every byte of the two outputs is written (tail sequences as all-'A').
+ * Errors: GK_ERR_ARG (NULL, n_seqs < 0, stride < len or > GK_MAX_STRIDE),
+ * GK_ERR_LEN, GK_ERR_ALIGN, GK_ERR_CUDA. */
+int gk_encode(const uint8_t* d_seqs, int64_t n_seqs, int32_t len, int64_t stride,
+              uint32_t* d_packed, uint32_t* d_undef, void* stream);
+
+/* a2-a6: the filtration of n_pairs packed pairs (read p = sequence p of
+ * d_reads_packed, reference segment p = sequence p of d_refs_packed; both sets
+ * encoded by gk_encode with the same n and len).
+ *  d_accept_bits : gk_result_words(n_pairs) u32 (written).
+ *  d_errcount    : n_pairs bytes (written) or NULL.
+ * Errors: GK_ERR_ARG, GK_ERR_LEN, GK_ERR_E, GK_ERR_ALIGN, GK_ERR_CUDA. */
+int gk_filter(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
+              const uint32_t* d_read_undef, const uint32_t* d_ref_undef,
+              int64_t n_pairs, int32_t len, int32_t e,
+              uint32_t* d_accept_bits, uint8_t* d_errcount, void* stream);
+
+/* gk_filter with option flags.  GK_FLAG_GENERIC forces the mask-major fallback
+ * kernel that otherwise only serves e above the register-resident instantiations
+ * (diagnostic / test knob: results are identical). */
+#define GK_FLAG_GENERIC 1
+int gk_filter_ex(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
+                 const uint32_t* d_read_undef, const uint32_t* d_ref_undef,
+                 int64_t n_pairs, int32_t len, int32_t e,
+                 uint32_t* d_accept_bits, uint8_t* d_errcount, int32_t flags, void* stream);
+
+/* a1-a6 in one launch from ASCII (the paper's "device-encoded" kernel, :105):
+ * same inputs as two gk_encode calls (reads and refs share `stride`), same
+ * outputs as gk_filter; no packed intermediate is written to HBM.
+ * Errors: as gk_encode + GK_ERR_E. */
+int gk_filter_ascii(const uint8_t* d_reads, const uint8_t* d_refs, int64_t stride,
+                    int64_t n_pairs, int32_t len, int32_t e,
+                    uint32_t* d_accept_bits, uint8_t* d_errcount, void* stream);
+
+/* a7: ordered indices of the accepted pairs (the accepted
+ * pairs go on to verification).
+ *  d_accept_bits : as written by gk_filter for n_pairs (n_pairs < 2^32).
+ *  d_idx         : room for n_pairs u32 (only the first *d_n_acc are written),
+ *                  ascending pair indices.  May be NULL to only count.
+ *  d_n_acc       : one u64 (written): the number of accepted pairs.
+ *  d_ws          : gk_compact_workspace_bytes(n_pairs) bytes of scratch.
+ * Errors: GK_ERR_ARG, GK_ERR_ALIGN, GK_ERR_WORKSPACE, GK_ERR_CUDA. */
+size_t gk_compact_workspace_bytes(int64_t n_pairs);
+int gk_compact(const uint32_t* d_accept_bits, int64_t n_pairs, uint32_t* d_idx,
+               uint64_t* d_n_acc, void* d_ws, size_t ws_bytes, void* stream);
+
+/* End-to-end from HOST buffers (the paper's "filter time"): streams
+ * the pairs through device memory in chunks, overlapping host->device copies,
+ * filtering and device->host copies on two CUDA streams.
+ *  h_reads, h_refs : n_pairs rows of `stride` bytes in host memory (pinned memory
+ *                    gives full PCIe / C2C bandwidth; pageable works).
+ *  h_accept_bits   : gk_result_words(n_pairs) u32 in host memory (written).
+ *  h_errcount      : n_pairs bytes in host memory (written) or NULL.
+ *  d_ws            : device scratch of gk_host_workspace_bytes(chunk_pairs, stride) bytes;
+ *                    chunk_pairs (a multiple of 1024, > 0) sets the pipeline granularity.
+ * Synchronous: returns after the results are in host memory.
+ * Errors: as gk_filter_ascii + GK_ERR_WORKSPACE. */
+size_t gk_host_workspace_bytes(int64_t chunk_pairs, int64_t stride);
+int gk_filter_host(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride,
+                   int64_t n_pairs, int32_t len, int32_t e,
+                   uint32_t* h_accept_bits, uint8_t* h_errcount,
+                   void* d_ws, size_t ws_bytes, int64_t chunk_pairs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GATEKEEPER_H */

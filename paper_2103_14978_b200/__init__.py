@@ -1,0 +1,193 @@
+"""paper_2103_14978_b200 -- B200-native GateKeeper-GPU pre-alignment filter.
+
+Thin Python binding over the C ABI of ``libgk.so`` (include/gatekeeper.h):
+argument marshalling only.  Every step of the filter runs in the library's
+CUDA kernels; there is no CPU path.  If ``libgk.so`` is missing or cannot be
+loaded, importing the functions below raises -- the product never falls back
+to anything else.
+
+Tensors are torch tensors (PyTorch provides device memory and streams only).
+Names follow the paper: ``encode``, ``filter`` /
+``filter_ascii`` (the filtration, :79, :105-109), ``compact`` (accepted pairs
+handed to verification, :166-168).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgk.so")
+GK_MAX_LEN = 508
+GK_MAX_STRIDE = 1024
+GK_TILE = 1024
+GK_FLAG_GENERIC = 1
+
+_lib = None
+
+
+class GateKeeperError(RuntimeError):
+    pass
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libgk.so and declare the C ABI.  Raises if the library is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise GateKeeperError(
+            f"{path} not found: build it with `python -m paper_2103_14978_b200._build` "
+            "(or __graft_entry__.build()); there is no fallback path")
+    lib = ctypes.CDLL(path)
+    P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    sig = {
+        "gk_version": (ctypes.c_int, []),
+        "gk_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+        "gk_last_cuda_error": (ctypes.c_int, []),
+        "gk_packed_words": (SZ, [I64, I32]),
+        "gk_undef_words": (SZ, [I64]),
+        "gk_result_words": (SZ, [I64]),
+        "gk_encode": (ctypes.c_int, [P, I64, I32, I64, P, P, P]),
+        "gk_filter": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, P]),
+        "gk_filter_ex": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, I32, P]),
+        "gk_filter_ascii": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P]),
+        "gk_compact_workspace_bytes": (SZ, [I64]),
+        "gk_compact": (ctypes.c_int, [P, I64, P, P, P, SZ, P]),
+        "gk_host_workspace_bytes": (SZ, [I64, I64]),
+        "gk_filter_host": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P, SZ, I64]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        lib = load_library()
+        msg = lib.gk_status_string(rc).decode()
+        if rc == -6:
+            msg += f" (cudaError {lib.gk_last_cuda_error()})"
+        raise GateKeeperError(f"{what} failed: {msg} [{rc}]")
+
+
+def _stream(stream=None):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+# ---- size queries -------------------------------------------------------------
+def packed_words(n: int, length: int) -> int:
+    return load_library().gk_packed_words(n, length)
+
+
+def undef_words(n: int) -> int:
+    return load_library().gk_undef_words(n)
+
+
+def result_words(n: int) -> int:
+    return load_library().gk_result_words(n)
+
+
+# ---- a1: encode ---------------------------------------------------------------
+def encode(seqs, length: int | None = None, out=None, stream=None):
+    """ASCII rows (uint8 CUDA tensor [n, stride]) -> (packed u32 words, undef u32 words)."""
+    import torch
+    n, stride = seqs.shape
+    length = stride if length is None else length
+    if out is None:
+        packed = torch.empty(packed_words(n, length), dtype=torch.int32, device=seqs.device)
+        undef = torch.empty(undef_words(n), dtype=torch.int32, device=seqs.device)
+    else:
+        packed, undef = out
+    _check(load_library().gk_encode(seqs.data_ptr(), n, length, stride, _ptr(packed), _ptr(undef),
+                                    _stream(stream)), "gk_encode")
+    return packed, undef
+
+
+# ---- a2..a6: filter -----------------------------------------------------------
+def filter(reads_packed, refs_packed, read_undef, ref_undef, n: int, length: int, e: int,
+           accept=None, errcount=None, want_errcount: bool = True, flags: int = 0,
+           stream=None):
+    """Filtration of n packed pairs -> (accept bits u32[ceil(n/32)], errcount u8[n] or None)."""
+    import torch
+    dev = reads_packed.device
+    if accept is None:
+        accept = torch.empty(max(1, result_words(n)), dtype=torch.int32, device=dev)
+    if errcount is None and want_errcount:
+        errcount = torch.empty(max(1, n), dtype=torch.uint8, device=dev)
+    _check(load_library().gk_filter_ex(_ptr(reads_packed), _ptr(refs_packed), _ptr(read_undef),
+                                       _ptr(ref_undef), n, length, e, _ptr(accept),
+                                       _ptr(errcount), flags, _stream(stream)), "gk_filter")
+    return accept, errcount
+
+
+def filter_ascii(reads, refs, e: int, length: int | None = None, accept=None, errcount=None,
+                 want_errcount: bool = True, stream=None):
+    """Fused a1..a6 from ASCII rows -> (accept bits, errcount or None)."""
+    import torch
+    n, stride = reads.shape
+    length = stride if length is None else length
+    if accept is None:
+        accept = torch.empty(max(1, result_words(n)), dtype=torch.int32, device=reads.device)
+    if errcount is None and want_errcount:
+        errcount = torch.empty(max(1, n), dtype=torch.uint8, device=reads.device)
+    _check(load_library().gk_filter_ascii(reads.data_ptr(), refs.data_ptr(), stride, n, length,
+                                          e, _ptr(accept), _ptr(errcount), _stream(stream)),
+           "gk_filter_ascii")
+    return accept, errcount
+
+
+# ---- a7: compact --------------------------------------------------------------
+def compact_workspace_bytes(n: int) -> int:
+    return load_library().gk_compact_workspace_bytes(n)
+
+
+def compact(accept, n: int, idx=None, n_acc=None, workspace=None, want_indices: bool = True,
+            stream=None):
+    """Ordered indices of accepted pairs -> (idx u32[n] (first n_acc valid), n_acc u64[1])."""
+    import torch
+    dev = accept.device
+    if idx is None and want_indices:
+        idx = torch.empty(max(1, n), dtype=torch.int32, device=dev)
+    if n_acc is None:
+        n_acc = torch.empty(1, dtype=torch.int64, device=dev)
+    wsb = compact_workspace_bytes(n)
+    if workspace is None:
+        workspace = torch.empty(max(1, wsb), dtype=torch.uint8, device=dev)
+    _check(load_library().gk_compact(accept.data_ptr(), n, _ptr(idx), n_acc.data_ptr(),
+                                     workspace.data_ptr(), workspace.numel(), _stream(stream)),
+           "gk_compact")
+    return idx, n_acc
+
+
+# ---- end to end from host buffers ----------------------------------------------
+def host_workspace_bytes(chunk_pairs: int, stride: int) -> int:
+    return load_library().gk_host_workspace_bytes(chunk_pairs, stride)
+
+
+def filter_host(reads, refs, e: int, length: int | None = None, accept=None, errcount=None,
+                workspace=None, chunk_pairs: int = 1 << 20):
+    """End-to-end filtration of HOST (CPU, ideally pinned) uint8 tensors; results in host memory."""
+    import torch
+    n, stride = reads.shape
+    length = stride if length is None else length
+    if accept is None:
+        accept = torch.empty(max(1, result_words(n)), dtype=torch.int32, pin_memory=True)
+    if workspace is None:
+        workspace = torch.empty(host_workspace_bytes(chunk_pairs, stride), dtype=torch.uint8,
+                                device="cuda")
+    _check(load_library().gk_filter_host(reads.data_ptr(), refs.data_ptr(), stride, n, length, e,
+                                         accept.data_ptr(), _ptr(errcount),
+                                         workspace.data_ptr(), workspace.numel(), chunk_pairs),
+           "gk_filter_host")
+    return accept, errcount

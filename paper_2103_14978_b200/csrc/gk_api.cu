@@ -1,0 +1,208 @@
+// gk_api.cu -- the C ABI (include/gatekeeper.h): host-side validation, then the
+// launches.  No global mutable state apart from the thread-local last CUDA error.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gatekeeper.h"
+#include "gk_kernels.cuh"
+
+static thread_local int g_last_cuda_error = 0;
+
+static int cuda_status(cudaError_t err) {
+  if (err == cudaSuccess) return GK_OK;
+  g_last_cuda_error = (int)err;
+  return GK_ERR_CUDA;
+}
+
+static int after_launch() { return cuda_status(cudaGetLastError()); }
+
+static bool aligned(const void* p, uintptr_t a) {
+  return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0;
+}
+
+extern "C" {
+
+int gk_version(void) { return 10000; }
+
+const char* gk_status_string(int status) {
+  switch (status) {
+    case GK_OK: return "ok";
+    case GK_ERR_ARG: return "invalid argument";
+    case GK_ERR_LEN: return "len outside [1, GK_MAX_LEN]";
+    case GK_ERR_E: return "e outside [0, len)";
+    case GK_ERR_ALIGN: return "misaligned buffer";
+    case GK_ERR_WORKSPACE: return "workspace missing or too small";
+    case GK_ERR_CUDA: return "CUDA error (see gk_last_cuda_error)";
+    default: return "unknown status";
+  }
+}
+
+int gk_last_cuda_error(void) { return g_last_cuda_error; }
+
+size_t gk_packed_words(int64_t n_seqs, int32_t len) {
+  if (n_seqs <= 0 || len <= 0) return 0;
+  return (size_t)((n_seqs + GK_TILE - 1) / GK_TILE) * (size_t)len * 64u;
+}
+
+size_t gk_undef_words(int64_t n_seqs) {
+  if (n_seqs <= 0) return 0;
+  return (size_t)((n_seqs + GK_TILE - 1) / GK_TILE) * 32u;
+}
+
+size_t gk_result_words(int64_t n_pairs) {
+  if (n_pairs <= 0) return 0;
+  return (size_t)((n_pairs + 31) / 32);
+}
+
+static int check_ascii(const void* p, int64_t n, int32_t len, int64_t stride) {
+  if (n < 0) return GK_ERR_ARG;
+  if (len < 1 || len > GK_MAX_LEN) return GK_ERR_LEN;
+  if (stride < len || stride > GK_MAX_STRIDE) return GK_ERR_ARG;
+  if (n > 0 && p == nullptr) return GK_ERR_ARG;
+  return GK_OK;
+}
+
+int gk_encode(const uint8_t* d_seqs, int64_t n_seqs, int32_t len, int64_t stride,
+              uint32_t* d_packed, uint32_t* d_undef, void* stream) {
+  int rc = check_ascii(d_seqs, n_seqs, len, stride);
+  if (rc) return rc;
+  if (n_seqs == 0) return GK_OK;
+  if (!d_packed || !d_undef) return GK_ERR_ARG;
+  if (!aligned(d_packed, 16) || !aligned(d_undef, 4)) return GK_ERR_ALIGN;
+  gk::launch_encode(d_seqs, n_seqs, len, stride, d_packed, d_undef, (cudaStream_t)stream);
+  return after_launch();
+}
+
+int gk_filter_ex(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
+                 const uint32_t* d_read_undef, const uint32_t* d_ref_undef, int64_t n_pairs,
+                 int32_t len, int32_t e, uint32_t* d_accept_bits, uint8_t* d_errcount,
+                 int32_t flags, void* stream) {
+  if (n_pairs < 0) return GK_ERR_ARG;
+  if (len < 1 || len > GK_MAX_LEN) return GK_ERR_LEN;
+  if (e < 0 || e >= len) return GK_ERR_E;
+  if (n_pairs == 0) return GK_OK;
+  if (!d_reads_packed || !d_refs_packed || !d_read_undef || !d_ref_undef || !d_accept_bits)
+    return GK_ERR_ARG;
+  if (!aligned(d_reads_packed, 16) || !aligned(d_refs_packed, 16) || !aligned(d_read_undef, 4) ||
+      !aligned(d_ref_undef, 4) || !aligned(d_accept_bits, 4))
+    return GK_ERR_ALIGN;
+  gk::launch_filter(d_reads_packed, d_refs_packed, d_read_undef, d_ref_undef, n_pairs, len, e,
+                    d_accept_bits, d_errcount, (flags & GK_FLAG_GENERIC) ? 1 : 0,
+                    (cudaStream_t)stream);
+  return after_launch();
+}
+
+int gk_filter(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
+              const uint32_t* d_read_undef, const uint32_t* d_ref_undef, int64_t n_pairs,
+              int32_t len, int32_t e, uint32_t* d_accept_bits, uint8_t* d_errcount,
+              void* stream) {
+  return gk_filter_ex(d_reads_packed, d_refs_packed, d_read_undef, d_ref_undef, n_pairs, len, e,
+                      d_accept_bits, d_errcount, 0, stream);
+}
+
+int gk_filter_ascii(const uint8_t* d_reads, const uint8_t* d_refs, int64_t stride,
+                    int64_t n_pairs, int32_t len, int32_t e, uint32_t* d_accept_bits,
+                    uint8_t* d_errcount, void* stream) {
+  int rc = check_ascii(d_reads, n_pairs, len, stride);
+  if (rc) return rc;
+  if (n_pairs > 0 && d_refs == nullptr) return GK_ERR_ARG;
+  if (e < 0 || e >= len) return GK_ERR_E;
+  if (n_pairs == 0) return GK_OK;
+  if (!d_accept_bits) return GK_ERR_ARG;
+  if (!aligned(d_accept_bits, 4)) return GK_ERR_ALIGN;
+  gk::launch_filter_ascii(d_reads, d_refs, stride, n_pairs, len, e, d_accept_bits, d_errcount,
+                          (cudaStream_t)stream);
+  return after_launch();
+}
+
+size_t gk_compact_workspace_bytes(int64_t n_pairs) {
+  return gk::compact_workspace_bytes(n_pairs < 0 ? 0 : n_pairs);
+}
+
+int gk_compact(const uint32_t* d_accept_bits, int64_t n_pairs, uint32_t* d_idx,
+               uint64_t* d_n_acc, void* d_ws, size_t ws_bytes, void* stream) {
+  if (n_pairs < 0 || n_pairs >= ((int64_t)1 << 32)) return GK_ERR_ARG;
+  if (!d_n_acc) return GK_ERR_ARG;
+  if (!aligned(d_n_acc, 8)) return GK_ERR_ALIGN;
+  if (n_pairs == 0) return cuda_status(cudaMemsetAsync(d_n_acc, 0, 8, (cudaStream_t)stream));
+  if (!d_accept_bits) return GK_ERR_ARG;
+  if (!aligned(d_accept_bits, 4) || (d_idx && !aligned(d_idx, 4))) return GK_ERR_ALIGN;
+  if (!d_ws || ws_bytes < gk::compact_workspace_bytes(n_pairs)) return GK_ERR_WORKSPACE;
+  gk::launch_compact(d_accept_bits, n_pairs, d_idx, d_n_acc, d_ws, (cudaStream_t)stream);
+  return after_launch();
+}
+
+// ---- host-buffer end-to-end pipeline ------------------------------------------
+static size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t gk_host_workspace_bytes(int64_t chunk_pairs, int64_t stride) {
+  if (chunk_pairs <= 0 || stride <= 0) return 0;
+  const size_t in = round_up((size_t)chunk_pairs * (size_t)stride, 256);
+  const size_t acc = round_up((size_t)(chunk_pairs / 32 + 1) * 4, 256);
+  const size_t err = round_up((size_t)chunk_pairs, 256);
+  return 2 * (2 * in + acc + err);
+}
+
+int gk_filter_host(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride,
+                   int64_t n_pairs, int32_t len, int32_t e, uint32_t* h_accept_bits,
+                   uint8_t* h_errcount, void* d_ws, size_t ws_bytes, int64_t chunk_pairs) {
+  int rc = check_ascii(h_reads, n_pairs, len, stride);
+  if (rc) return rc;
+  if (e < 0 || e >= len) return GK_ERR_E;
+  if (n_pairs == 0) return GK_OK;
+  if (!h_refs || !h_accept_bits) return GK_ERR_ARG;
+  if (chunk_pairs <= 0 || chunk_pairs % 1024 != 0) return GK_ERR_ARG;
+  if (!d_ws || ws_bytes < gk_host_workspace_bytes(chunk_pairs, stride)) return GK_ERR_WORKSPACE;
+  if (!aligned(d_ws, 256)) return GK_ERR_ALIGN;
+
+  const size_t in = round_up((size_t)chunk_pairs * (size_t)stride, 256);
+  const size_t acc = round_up((size_t)(chunk_pairs / 32 + 1) * 4, 256);
+  const size_t errb = round_up((size_t)chunk_pairs, 256);
+  uint8_t* base = static_cast<uint8_t*>(d_ws);
+  struct Buf { uint8_t *r, *f; uint32_t* a; uint8_t* c; } buf[2];
+  for (int b = 0; b < 2; ++b) {
+    uint8_t* p = base + b * (2 * in + acc + errb);
+    buf[b].r = p;
+    buf[b].f = p + in;
+    buf[b].a = reinterpret_cast<uint32_t*>(p + 2 * in);
+    buf[b].c = p + 2 * in + acc;
+  }
+  cudaStream_t st[2];
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t err = cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking);
+    if (err != cudaSuccess) {
+      if (b == 1) cudaStreamDestroy(st[0]);
+      return cuda_status(err);
+    }
+  }
+  rc = GK_OK;
+  const int64_t nchunks = (n_pairs + chunk_pairs - 1) / chunk_pairs;
+  for (int64_t c = 0; c < nchunks && rc == GK_OK; ++c) {
+    const int b = (int)(c & 1);
+    const int64_t p0 = c * chunk_pairs;
+    const int64_t np = (n_pairs - p0) < chunk_pairs ? (n_pairs - p0) : chunk_pairs;
+    const size_t bytes = (size_t)((np - 1) * stride + len);
+    cudaError_t err = cudaMemcpyAsync(buf[b].r, h_reads + p0 * stride, bytes,
+                                      cudaMemcpyHostToDevice, st[b]);
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(buf[b].f, h_refs + p0 * stride, bytes, cudaMemcpyHostToDevice, st[b]);
+    if (err != cudaSuccess) { rc = cuda_status(err); break; }
+    gk::launch_filter_ascii(buf[b].r, buf[b].f, stride, np, len, e, buf[b].a,
+                            h_errcount ? buf[b].c : nullptr, st[b]);
+    rc = after_launch();
+    if (rc) break;
+    err = cudaMemcpyAsync(h_accept_bits + p0 / 32, buf[b].a, (size_t)((np + 31) / 32) * 4,
+                          cudaMemcpyDeviceToHost, st[b]);
+    if (err == cudaSuccess && h_errcount)
+      err = cudaMemcpyAsync(h_errcount + p0, buf[b].c, (size_t)np, cudaMemcpyDeviceToHost, st[b]);
+    if (err != cudaSuccess) { rc = cuda_status(err); break; }
+  }
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t err = cudaStreamSynchronize(st[b]);
+    if (rc == GK_OK && err != cudaSuccess) rc = cuda_status(err);
+    cudaStreamDestroy(st[b]);
+  }
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// gk_compact.cu -- a7: ordered indices of the accepted pairs.
+//
+// The paper's host scans the result buffer for '1's before verification
+// (PAPER.md:166-168).  Here the accept bits (one u32 per 32 pairs, as written by
+// gk_filter) are compacted on the device: pass 1 counts the set bits of each
+// CTA's chunk (popc), pass 2 re-reads the chunk, turns the per-CTA totals into
+// its global offset and writes every accepted pair index in ascending order
+// (a per-thread exclusive scan of popc, then one index per set bit).
+#include "gk_common.cuh"
+#include "gk_kernels.cuh"
+
+namespace gk {
+
+constexpr int CP_THREADS = 256;
+constexpr int CP_WORDS_PER_THREAD = 8;
+constexpr int CP_WORDS_PER_CTA = CP_THREADS * CP_WORDS_PER_THREAD;  // 65536 pairs
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* sm_warp,
+                                                         uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) sm_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < (CP_THREADS / 32) ? sm_warp[lane] : 0u;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, d);
+      if (lane >= d) w += y;
+    }
+    if (lane < (CP_THREADS / 32)) sm_warp[lane] = w;
+  }
+  __syncthreads();
+  total = sm_warp[CP_THREADS / 32 - 1];
+  const uint32_t before = warp > 0 ? sm_warp[warp - 1] : 0u;
+  return before + x - v;
+}
+
+__device__ __forceinline__ uint32_t load_word(const uint32_t* bits, int64_t w, int64_t nwords,
+                                              int64_t n) {
+  if (w >= nwords) return 0u;
+  uint32_t v = __ldg(bits + w);
+  const int64_t first = w * 32;
+  if (first + 32 > n) v &= (1u << (int)(n - first)) - 1u;  // bits >= n are ignored
+  return v;
+}
+
+__global__ void __launch_bounds__(CP_THREADS) compact_count_kernel(const uint32_t* __restrict__ bits,
+                                                                   int64_t n,
+                                                                   uint32_t* __restrict__ cta_counts) {
+  __shared__ uint32_t sm[CP_THREADS / 32];
+  const int64_t nwords = (n + 31) / 32;
+  const int64_t w0 = (int64_t)blockIdx.x * CP_WORDS_PER_CTA + threadIdx.x;
+  uint32_t c = 0u;
+#pragma unroll
+  for (int t = 0; t < CP_WORDS_PER_THREAD; ++t)
+    c += __popc(load_word(bits, w0 + (int64_t)t * CP_THREADS, nwords, n));
+  uint32_t total;
+  block_exclusive_scan(c, sm, total);
+  if (threadIdx.x == 0) cta_counts[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(CP_THREADS) compact_write_kernel(
+    const uint32_t* __restrict__ bits, int64_t n, const uint32_t* __restrict__ cta_counts,
+    uint32_t* __restrict__ idx, unsigned long long* __restrict__ n_acc) {
+  __shared__ uint32_t sm[CP_THREADS / 32];
+  __shared__ unsigned long long sm_base;
+  const int64_t nwords = (n + 31) / 32;
+  // global offset of this CTA: sum of the totals of all previous CTAs
+  unsigned long long part = 0ull;
+  for (unsigned b = threadIdx.x; b < blockIdx.x; b += CP_THREADS) part += cta_counts[b];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) part += __shfl_down_sync(0xFFFFFFFFu, part, d);
+  __shared__ unsigned long long sm_part[CP_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) sm_part[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0ull;
+    for (int w = 0; w < CP_THREADS / 32; ++w) s += sm_part[w];
+    sm_base = s;
+  }
+  // each thread owns CP_WORDS_PER_THREAD consecutive words (ascending order)
+  const int64_t w0 = (int64_t)blockIdx.x * CP_WORDS_PER_CTA + (int64_t)threadIdx.x * CP_WORDS_PER_THREAD;
+  uint32_t words[CP_WORDS_PER_THREAD];
+  uint32_t c = 0u;
+#pragma unroll
+  for (int t = 0; t < CP_WORDS_PER_THREAD; ++t) {
+    words[t] = load_word(bits, w0 + t, nwords, n);
+    c += __popc(words[t]);
+  }
+  uint32_t total;
+  const uint32_t off = block_exclusive_scan(c, sm, total);
+  const unsigned long long base = sm_base;
+  if (idx != nullptr) {
+    unsigned long long o = base + off;
+#pragma unroll
+    for (int t = 0; t < CP_WORDS_PER_THREAD; ++t) {
+      uint32_t v = words[t];
+      const uint32_t pbase = (uint32_t)((w0 + t) * 32);
+      while (v) {
+        const int b = __ffs(v) - 1;
+        idx[o++] = pbase + (uint32_t)b;
+        v &= v - 1u;
+      }
+    }
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *n_acc = base + total;
+}
+
+size_t compact_workspace_bytes(int64_t n) {
+  const int64_t nwords = (n + 31) / 32;
+  const int64_t ctas = (nwords + CP_WORDS_PER_CTA - 1) / CP_WORDS_PER_CTA;
+  return (size_t)(ctas > 0 ? ctas : 1) * sizeof(uint32_t);
+}
+
+int launch_compact(const uint32_t* bits, int64_t n, uint32_t* idx, uint64_t* n_acc, void* ws,
+                   cudaStream_t stream) {
+  const int64_t nwords = (n + 31) / 32;
+  const int64_t ctas = (nwords + CP_WORDS_PER_CTA - 1) / CP_WORDS_PER_CTA;
+  uint32_t* counts = reinterpret_cast<uint32_t*>(ws);
+  compact_count_kernel<<<(unsigned)ctas, CP_THREADS, 0, stream>>>(bits, n, counts);
+  compact_write_kernel<<<(unsigned)ctas, CP_THREADS, 0, stream>>>(
+      bits, n, counts, idx, reinterpret_cast<unsigned long long*>(n_acc));
+  return 0;
+}
+
+}  // namespace gk

@@ -1,0 +1,122 @@
+// gk_encode_core.cuh -- device functions of a1 (ASCII -> bit-sliced 2-bit planes),
+// shared by gk_encode (encode_kernel) and the fused gk_filter_ascii kernel.
+// See gk_encode.cu for the method notes.
+#pragma once
+#include "gk_common.cuh"
+
+namespace gk {
+
+// bit 2 of bytes 0..3 -> bits 28..31.  Partial products land on bit
+// 28 + 8j - 7k (byte j, multiplier term k): == 28+k for j == k, >= 36 (dropped)
+// for j > k, and on the distinct bits {7,14,15,21,22,23} for j < k: no carries.
+__device__ __forceinline__ uint32_t gather_bit2(uint32_t r) { return (r & 0x04040404u) * 0x04081020u; }
+// bit 1 of bytes 0..3 -> bits 28..31 (same argument, terms shifted by one).
+__device__ __forceinline__ uint32_t gather_bit1(uint32_t r) { return (r & 0x02020202u) * 0x08102040u; }
+
+// 0 iff all 4 bytes of w are in {A,C,G,T,a,c,g,t}.
+__device__ __forceinline__ uint32_t invalid_bytes(uint32_t w) {
+  uint32_t base = (w & 0x26262626u) | 0x41414141u;
+  uint32_t tflag = (w >> 2) & ~(w >> 1) & 0x01010101u;
+  return w ^ (base + 15u * tflag);
+}
+
+// 4 bytes of smem row starting at byte offset `off` (any alignment).
+template <bool ALIGNED>
+__device__ __forceinline__ uint32_t lds_u32(const uint8_t* sm, uint32_t off) {
+  if (ALIGNED) return *reinterpret_cast<const uint32_t*>(sm + off);
+  uint32_t a = off & ~3u;
+  uint32_t lo = *reinterpret_cast<const uint32_t*>(sm + a);
+  uint32_t hi = *reinterpret_cast<const uint32_t*>(sm + a + 4);
+  return __funnelshift_r(lo, hi, (off & 3u) * 8u);
+}
+
+// Cooperative copy of bytes [src, src+nbytes) into smem so that global address
+// a lands at sm[a - (src & ~15)]; 16-byte vector loads for the aligned middle.
+__device__ __forceinline__ void stage_span(const uint8_t* src, int64_t nbytes, uint8_t* sm,
+                                           int tid, int nthr) {
+  uintptr_t a0 = reinterpret_cast<uintptr_t>(src);
+  uintptr_t abase = a0 & ~uintptr_t(15);
+  uintptr_t a1 = a0 + nbytes;
+  uintptr_t m0 = (a0 + 15) & ~uintptr_t(15);
+  uintptr_t m1 = a1 & ~uintptr_t(15);
+  if (m0 > a1) m0 = a1;
+  if (m1 < m0) m1 = m0;
+  for (uintptr_t a = a0 + tid; a < m0; a += nthr)
+    sm[a - abase] = *reinterpret_cast<const uint8_t*>(a);
+  const int64_t nvec = (int64_t)((m1 - m0) >> 4);
+  const uint4* gv = reinterpret_cast<const uint4*>(m0);
+  uint4* sv = reinterpret_cast<uint4*>(sm + (m0 - abase));
+  for (int64_t v = tid; v < nvec; v += nthr) sv[v] = __ldg(gv + v);
+  for (uintptr_t a = m1 + tid; a < a1; a += nthr)
+    sm[a - abase] = *reinterpret_cast<const uint8_t*>(a);
+}
+
+// Encode the 32 sequences of one group whose rows start in smem at
+// sm + row0_off + s*stride (s = 0..31; rows >= nvalid are all-'A').
+// Lane q handles base positions 4q..4q+3 (q = lane, lane+32, ...).
+// emit(pos, hi_word, lo_word) is called for every position < len.
+// Returns the group's undefined-sequence word (valid in all lanes).
+template <bool ALIGNED, typename Emit>
+__device__ __forceinline__ uint32_t encode_group(const uint8_t* sm, uint32_t row0_off,
+                                                 uint32_t stride, int nvalid, int len,
+                                                 Emit&& emit) {
+  const int lane = threadIdx.x & 31;
+  const int nquads = (len + 3) >> 2;
+  uint32_t bad[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) bad[b] = 0u;
+
+  for (int q = lane; q < nquads; q += 32) {
+    uint32_t hb[4] = {0u, 0u, 0u, 0u}, lb[4] = {0u, 0u, 0u, 0u};
+    const int rem = len - 4 * q;  // >= 1
+    // byte mask of positions < len inside this quad
+    const uint32_t posmask = rem >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (8 * (4 - rem)));
+#pragma unroll
+    for (int blk = 7; blk >= 0; --blk) {
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int s = 4 * blk + k;
+        w[k] = s < nvalid ? lds_u32<ALIGNED>(sm, row0_off + (uint32_t)s * stride + 4u * q)
+                          : 0x41414141u;
+      }
+      // validity of the 16 bytes (only positions < len)
+      uint32_t e4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) e4[k] = invalid_bytes(w[k]) & posmask;
+      // byte transpose: r[m] byte k = w[k] byte m
+      const uint32_t t0 = __byte_perm(w[0], w[1], 0x5140);
+      const uint32_t t1 = __byte_perm(w[0], w[1], 0x7362);
+      const uint32_t t2 = __byte_perm(w[2], w[3], 0x5140);
+      const uint32_t t3 = __byte_perm(w[2], w[3], 0x7362);
+      uint32_t r[4];
+      r[0] = __byte_perm(t0, t2, 0x5410);
+      r[1] = __byte_perm(t0, t2, 0x7632);
+      r[2] = __byte_perm(t1, t3, 0x5410);
+      r[3] = __byte_perm(t1, t3, 0x7632);
+      // per-sequence error flags: fold the 4 positions of each row into byte k
+      uint32_t ek = 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ek |= (e4[k] != 0u ? 1u : 0u) << (8 * k);
+      bad[blk] |= ek;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        hb[m] = __funnelshift_l(gather_bit2(r[m]), hb[m], 4);
+        lb[m] = __funnelshift_l(gather_bit1(r[m]), lb[m], 4);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (m < rem) emit(4 * q + m, hb[m], hb[m] ^ lb[m]);
+  }
+  uint32_t und = 0u;
+#pragma unroll
+  for (int blk = 0; blk < 8; ++blk) {
+    const uint32_t b = __reduce_or_sync(0xFFFFFFFFu, bad[blk]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) und |= ((b >> (8 * k)) & 1u) << (4 * blk + k);
+  }
+  return und;
+}
+
+}  // namespace gk

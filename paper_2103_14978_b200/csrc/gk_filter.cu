@@ -1,0 +1,110 @@
+// gk_filter.cu -- a2..a6: the filtration of packed pairs (gk_filter).
+//
+// Launch geometry: one warp per tile of 1024 pairs, one lane per group of 32
+// pairs (lane g reads the words of group g: 32 lanes x 8 bytes = 256 contiguous
+// bytes per base position, so every load instruction of the warp is one fully
+// used 256-byte segment).  The paper runs one filtration per thread (:79); here
+// one thread runs 32 filtrations at once, one per bit of every word.
+//
+// Two kernels:
+//   * filter_sp<E>  (e == E <= GK_SP_EMAX): single pass, everything in registers
+//     (gk_filter_core.cuh).  Positions are split into checked head/tail steps and
+//     an unchecked middle that is unrolled by 8 (static carry-save count tree).
+//   * filter_generic (any e): mask-major, F kept in shared memory, one mask at a
+//     time; the fallback for e > GK_SP_EMAX.
+#include "gk_common.cuh"
+#include "gk_filter_core.cuh"
+#include "gk_kernels.cuh"
+
+namespace gk {
+
+template <int E>
+__global__ void __launch_bounds__(128) filter_sp_kernel(
+    const uint2* __restrict__ reads, const uint2* __restrict__ refs,
+    const uint32_t* __restrict__ rund, const uint32_t* __restrict__ fund, int64_t n, int len,
+    uint32_t* __restrict__ accept, uint8_t* __restrict__ errc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t g = tile * 32 + lane;
+  if (g * 32 >= n) return;
+  GlobalGroupSrc src;
+  src.q = reads + tile * (int64_t)len * 32 + lane;
+  src.r = refs + tile * (int64_t)len * 32 + lane;
+  src.len = len;
+
+  SinglePass<E> sp;
+  run_range<E>(sp, src, len, 0, len);
+  uint32_t cA[8], cF[8];
+  sp.cA.planes(cA);
+  sp.cF.planes(cF);
+  finish_group(cA, cF, E, __ldg(rund + g) | __ldg(fund + g), g, n, accept, errc);
+}
+
+// ---------------------------------------------------------------------------
+// Generic fallback: mask-major, F[pos][lane] in shared memory.
+__global__ void __launch_bounds__(128) filter_generic_kernel(
+    const uint2* __restrict__ reads, const uint2* __restrict__ refs,
+    const uint32_t* __restrict__ rund, const uint32_t* __restrict__ fund, int64_t n, int len,
+    int e, uint32_t* __restrict__ accept, uint8_t* __restrict__ errc) {
+  extern __shared__ uint32_t sm_f[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int64_t g = tile * 32 + lane;
+  if (g * 32 >= n) return;
+  GlobalGroupSrc src;
+  src.q = reads + tile * (int64_t)len * 32 + lane;
+  src.r = refs + tile * (int64_t)len * 32 + lane;
+  src.len = len;
+  const uint32_t undef = __ldg(rund + g) | __ldg(fund + g);
+  uint32_t cA[8], cF[8];
+  generic_group(src, len, e, undef, sm_f + (size_t)warp * len * 32 + lane, 32, cA, cF);
+  finish_group(cA, cF, e, undef, g, n, accept, errc);
+}
+
+template <int E>
+static void launch_sp(const uint2* reads, const uint2* refs, const uint32_t* rund,
+                      const uint32_t* fund, int64_t n, int len, uint32_t* accept, uint8_t* errc,
+                      cudaStream_t stream) {
+  const int64_t tiles = (n + 1023) / 1024;
+  const int warps = 4;
+  const int64_t blocks = (tiles + warps - 1) / warps;
+  filter_sp_kernel<E><<<(unsigned)blocks, warps * 32, 0, stream>>>(reads, refs, rund, fund, n,
+                                                                    len, accept, errc);
+}
+
+template <int E>
+static bool dispatch_sp(int e, const uint2* reads, const uint2* refs, const uint32_t* rund,
+                        const uint32_t* fund, int64_t n, int len, uint32_t* accept,
+                        uint8_t* errc, cudaStream_t stream) {
+  if (e == E) {
+    launch_sp<E>(reads, refs, rund, fund, n, len, accept, errc, stream);
+    return true;
+  }
+  if constexpr (E > 0) return dispatch_sp<E - 1>(e, reads, refs, rund, fund, n, len, accept, errc, stream);
+  return false;
+}
+
+int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* rund,
+                  const uint32_t* fund, int64_t n, int len, int e, uint32_t* accept,
+                  uint8_t* errc, int force_generic, cudaStream_t stream) {
+  const uint2* r2 = reinterpret_cast<const uint2*>(reads);
+  const uint2* f2 = reinterpret_cast<const uint2*>(refs);
+  if (!force_generic &&
+      dispatch_sp<GK_SP_EMAX>(e, r2, f2, rund, fund, n, len, accept, errc, stream))
+    return 0;
+  const int64_t tiles = (n + 1023) / 1024;
+  int warps = (int)(48 * 1024 / (len * 32 * 4));
+  if (warps > 4) warps = 4;
+  if (warps < 1) warps = 1;
+  const size_t smem = (size_t)warps * len * 32 * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(filter_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  const int64_t blocks = (tiles + warps - 1) / warps;
+  filter_generic_kernel<<<(unsigned)blocks, warps * 32, smem, stream>>>(r2, f2, rund, fund, n,
+                                                                        len, e, accept, errc);
+  return 0;
+}
+
+}  // namespace gk

@@ -1,0 +1,26 @@
+// gk_kernels.cuh -- internal launch entry points (C++; the C ABI is in gk_api.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef GK_SP_EMAX
+#define GK_SP_EMAX 11  // largest e with an all-register single-pass filter instantiation
+#endif
+
+namespace gk {
+
+int launch_encode(const uint8_t* seqs, int64_t n, int len, int64_t stride, uint32_t* packed,
+                  uint32_t* undef, cudaStream_t stream);
+
+int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* rund,
+                  const uint32_t* fund, int64_t n, int len, int e, uint32_t* accept,
+                  uint8_t* errc, int force_generic, cudaStream_t stream);
+
+int launch_filter_ascii(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n,
+                        int len, int e, uint32_t* accept, uint8_t* errc, cudaStream_t stream);
+
+size_t compact_workspace_bytes(int64_t n);
+int launch_compact(const uint32_t* bits, int64_t n, uint32_t* idx, uint64_t* n_acc, void* ws,
+                   cudaStream_t stream);
+
+}  // namespace gk

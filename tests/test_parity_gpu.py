@@ -1,0 +1,235 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bit-exact in every compared value: packed words and undefined flags of
+gk_encode, every accept bit and error count of gk_filter / gk_filter_ascii /
+gk_filter_host, and the index list of gk_compact.  Inputs are the seeded
+synthetic pairs of pairgen plus adversarial sets.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import pairgen
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def gk():
+    import paper_2103_14978_b200 as m
+    from paper_2103_14978_b200 import _build
+    _build.build()
+    m.load_library()
+    assert torch.cuda.is_available()
+    return m
+
+
+def to_dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def unpack_accept(words, n: int) -> np.ndarray:
+    w = words.cpu().numpy().astype(np.uint32).view(np.uint8)
+    return np.unpackbits(w, bitorder="little")[:n]
+
+
+def run_filter(gk, reads, refs, e, L=None, flags=0, path="packed"):
+    n, stride = reads.shape
+    L = stride if L is None else L
+    dr, df = to_dev(reads), to_dev(refs)
+    if path == "packed":
+        q, uq = gk.encode(dr, L)
+        r, ur = gk.encode(df, L)
+        acc, err = gk.filter(q, r, uq, ur, n, L, e, flags=flags)
+    elif path == "ascii":
+        acc, err = gk.filter_ascii(dr, df, e, L)
+    else:
+        raise ValueError(path)
+    torch.cuda.synchronize()
+    return unpack_accept(acc, n), err.cpu().numpy()[:n]
+
+
+def assert_parity(gk, reads, refs, e, L=None, flags=0, path="packed"):
+    a, c = run_filter(gk, reads, refs, e, L, flags, path)
+    oa, oc = oracle.filter(reads, refs, e, L)
+    bad = np.nonzero((a != oa) | (c != oc))[0]
+    assert bad.size == 0, (f"{bad.size} mismatches (L={L}, e={e}, path={path}, flags={flags}); "
+                           f"first: {[(int(i), int(a[i]), int(oa[i]), int(c[i]), int(oc[i])) for i in bad[:5]]}")
+    return oa, oc
+
+
+# ---------------------------------------------------------------- encode -------
+@pytest.mark.parametrize("L,n,stride,offset", [
+    (100, 3000, 100, 0), (1, 40, 1, 0), (2, 33, 2, 0), (3, 1025, 5, 0), (31, 100, 31, 1),
+    (32, 2048, 32, 0), (33, 999, 40, 3), (150, 1500, 150, 0), (150, 700, 160, 7),
+    (250, 2100, 256, 0), (508, 300, 508, 0), (508, 64, 1024, 5), (17, 5000, 17, 2)])
+def test_encode_matches_reference_packer(gk, L, n, stride, offset):
+    reads, _ = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, stride=stride,
+                                 emax=max(1, L // 10))
+    # random raw bytes in a few rows: every byte value must be classified
+    rng = np.random.default_rng(L * 7 + n)
+    rows = rng.choice(n, size=min(n, 20), replace=False)
+    reads[rows, :L] = rng.integers(0, 256, size=(rows.size, L), dtype=np.uint8)
+    buf = np.zeros(n * stride + offset + 16, dtype=np.uint8)
+    buf[offset:offset + n * stride] = reads.ravel()
+    dbuf = to_dev(buf)
+    seqs = dbuf[offset:offset + n * stride].view(n, stride)
+    words, und = gk.encode(seqs, L)
+    torch.cuda.synchronize()
+    ow, ou = oracle.pack(reads, L)
+    gw = words.cpu().numpy().astype(np.uint32)
+    gu = und.cpu().numpy().astype(np.uint32)
+    assert (gu == ou).all()
+    # plane bits are specified only for defined sequences
+    tiles = ou.size // 32
+    defined = ~np.repeat(ou.reshape(tiles, 1, 32, 1), L, axis=1).repeat(2, axis=3).reshape(-1)
+    assert ((gw & defined) == (ow & defined)).all()
+
+
+# ---------------------------------------------------------------- filter -------
+def test_c1_config_10k_100bp_e2(gk):
+    """BASELINE configs[0]: 10k synthetic pairs, 100 bp, e = 2."""
+    reads, refs = pairgen.gen_pairs(10_000, 100, profile=pairgen.PROFILE_BALANCED, emax=2)
+    for path in ("packed", "ascii"):
+        oa, oc = assert_parity(gk, reads, refs, 2, path=path)
+    dist = oracle.edit_distance(reads, refs)
+    defined = oc != 255
+    assert ((oa == 0) & (dist <= 2) & defined).sum() == 0   # no false rejects
+
+
+@pytest.mark.parametrize("L", [100, 150, 250])
+def test_paper_profile_e_sweep(gk, L):
+    n = 4000
+    reads, refs = pairgen.gen_pairs(n, L, seed=pairgen.SEED + L)
+    emax = {100: 10, 150: 15, 250: 25}[L]
+    oa, oc = oracle.sweep(reads, refs, emax)
+    for e in range(emax + 1):
+        for path, flags in (("packed", 0), ("ascii", 0), ("packed", 1)):
+            if flags and e % 3:
+                continue
+            a, c = run_filter(gk, reads, refs, e, flags=flags, path=path)
+            bad = np.nonzero((a != oa[e]) | (c != oc[e]))[0]
+            assert bad.size == 0, (L, e, path, flags, bad[:5])
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 31, 32, 33, 63, 64, 65, 127, 129, 255, 300, 508])
+def test_random_lengths(gk, L):
+    n = 1100 if L < 300 else 600
+    reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, emax=max(1, L // 10),
+                                    seed=L)
+    es = sorted({0, 1, min(2, L - 1), L // 10, min(L - 1, 13), min(L - 1, 20), L - 1})
+    for e in es:
+        assert_parity(gk, reads, refs, e, path="packed")
+        assert_parity(gk, reads, refs, e, path="ascii")
+
+
+def test_adversarial_sets(gk):
+    L = 48
+    rng = np.random.default_rng(1)
+    base = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, (512, L))]
+    sets = []
+    sets.append((base.copy(), base.copy()))                                     # identical
+    sets.append((np.full((256, L), ord("A"), np.uint8), np.full((256, L), ord("C"), np.uint8)))
+    alt = np.tile(np.frombuffer(b"AC", np.uint8), (256, L // 2))
+    sets.append((alt, np.roll(alt, 1, axis=1)))                                  # alternating
+    q = base.copy(); q[:, :3] = ord("T"); sets.append((q, base.copy()))          # edits at the start
+    q = base.copy(); q[:, -3:] = ord("G"); sets.append((q, base.copy()))         # edits at the end
+    q = np.roll(base, 1, axis=1); sets.append((q, base.copy()))                  # shifted by one
+    q = np.roll(base, -5, axis=1); sets.append((q, base.copy()))
+    q = base.copy(); q[::7, 10] = ord("N"); sets.append((q, base.copy()))        # undefined
+    q = base.copy() | 0x20; sets.append((q, base.copy()))                        # lower case
+    for reads, refs in sets:
+        for e in (0, 1, 2, 4, 8, 15, 23, 47):
+            assert_parity(gk, reads, refs, e, path="packed")
+            assert_parity(gk, reads, refs, e, path="ascii")
+
+
+def test_ragged_counts(gk):
+    L = 100
+    for n in (1, 31, 32, 33, 1023, 1024, 1025, 4097):
+        reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, emax=4, seed=n)
+        for e in (0, 3, 14):
+            assert_parity(gk, reads, refs, e, path="packed")
+            assert_parity(gk, reads, refs, e, path="ascii")
+
+
+def test_no_errcount_output(gk):
+    reads, refs = pairgen.gen_pairs(3000, 100)
+    dr, df = to_dev(reads), to_dev(refs)
+    q, uq = gk.encode(dr)
+    r, ur = gk.encode(df)
+    acc, err = gk.filter(q, r, uq, ur, 3000, 100, 5, want_errcount=False)
+    acc2, _ = gk.filter_ascii(dr, df, 5, want_errcount=False)
+    torch.cuda.synchronize()
+    assert err is None
+    oa, _ = oracle.filter(reads, refs, 5)
+    assert (unpack_accept(acc, 3000) == oa).all() and (unpack_accept(acc2, 3000) == oa).all()
+
+
+# ---------------------------------------------------------------- compact ------
+@pytest.mark.parametrize("n", [1, 77, 4096, 70_001, 300_000])
+def test_compact_indices(gk, n):
+    rng = np.random.default_rng(n)
+    bits = (rng.random(n) < 0.3).astype(np.uint8)
+    words = np.packbits(np.concatenate([bits, np.zeros((-n) % 32, np.uint8)]),
+                        bitorder="little").view(np.uint32)
+    dw = to_dev(words.view(np.int32))
+    idx, n_acc = gk.compact(dw, n)
+    torch.cuda.synchronize()
+    expect = np.nonzero(bits)[0]
+    assert int(n_acc.item()) == expect.size
+    assert (idx.cpu().numpy()[:expect.size].astype(np.uint32) == expect).all()
+
+
+def test_compact_after_filter(gk):
+    reads, refs = pairgen.gen_pairs(20_000, 150)
+    dr, df = to_dev(reads), to_dev(refs)
+    acc, _ = gk.filter_ascii(dr, df, 8)
+    idx, n_acc = gk.compact(acc, 20_000)
+    torch.cuda.synchronize()
+    oa, _ = oracle.filter(reads, refs, 8)
+    expect = np.nonzero(oa)[0]
+    assert int(n_acc.item()) == expect.size
+    assert (idx.cpu().numpy()[:expect.size] == expect).all()
+
+
+# ---------------------------------------------------------------- host e2e -----
+def test_filter_host_end_to_end(gk):
+    n, L = 50_000, 100
+    reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, emax=5)
+    hr = torch.from_numpy(reads).pin_memory()
+    hf = torch.from_numpy(refs).pin_memory()
+    err = torch.empty(n, dtype=torch.uint8).pin_memory()
+    acc, _ = gk.filter_host(hr, hf, 5, errcount=err, chunk_pairs=8192)
+    oa, oc = oracle.filter(reads, refs, 5)
+    assert (unpack_accept(acc, n) == oa).all()
+    assert (err.numpy() == oc).all()
+
+
+# ---------------------------------------------------------------- full size ----
+@pytest.mark.parametrize("L,e", [(100, 5), (150, 7), (250, 12)])
+def test_full_size_sampled(gk, L, e):
+    """30M-pair configurations at the launch configuration bench.py times:
+    device-generated inputs, outputs compared on sampled chunks that the oracle
+    recomputes from the same seeded generator."""
+    n = 30_000_000 if L == 100 else 10_000_000
+    dr, df = pairgen.gen_pairs_cuda(n, L)
+    acc, err = gk.filter_ascii(dr, df, e)
+    q, uq = gk.encode(dr, L)
+    r, ur = gk.encode(df, L)
+    acc2, err2 = gk.filter(q, r, uq, ur, n, L, e)
+    torch.cuda.synchronize()
+    assert torch.equal(acc, acc2) and torch.equal(err, err2)
+    rng = np.random.default_rng(L)
+    starts = sorted(rng.integers(0, n - 4096, size=6).tolist()) + [n - 4096]
+    acc_all = acc.cpu().numpy().astype(np.uint32)
+    err_all = err.cpu().numpy()
+    for s in starts:
+        s = (s // 32) * 32
+        reads, refs = pairgen.gen_pairs(4096, L, idx0=s)
+        oa, oc = oracle.filter(reads, refs, e)
+        bits = np.unpackbits(acc_all[s // 32:(s + 4096) // 32].view(np.uint8), bitorder="little")
+        assert (bits == oa).all() and (err_all[s:s + 4096] == oc).all(), s
+    del dr, df, q, r
