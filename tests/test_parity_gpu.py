@@ -119,7 +119,7 @@ def test_random_lengths(gk, L):
     n = 1100 if L < 300 else 600
     reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, emax=max(1, L // 10),
                                     seed=L)
-    es = sorted({0, 1, min(2, L - 1), L // 10, min(L - 1, 13), min(L - 1, 20), L - 1})
+    es = sorted(e for e in {0, 1, 2, L // 10, 13, 20, L - 1} if e < L)
     for e in es:
         assert_parity(gk, reads, refs, e, path="packed")
         assert_parity(gk, reads, refs, e, path="ascii")
