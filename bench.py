@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the GateKeeper-GPU hot path on B200 (one JSON line).
+
+Default (N=1): BASELINE.json configs[1] -- 30M synthetic pairs of 100 bp, error
+threshold swept e = 0..10.  One step = the whole hot path (SURVEY.md 8(a)
+a1..a7) over the batch for every e of the sweep: gk_encode of the reads and of
+the reference segments (a1, independent of e, once per step), then per e
+gk_filter (a2..a6: Hamming / shifted masks, amendment, edge fix, AND, windowed
+count, decision) and gk_compact (a7: ordered indices of the accepted pairs).
+--path fused runs gk_filter_ascii (a1..a6 in one kernel, re-encoding for every
+e) + gk_compact instead.  The metric is filtrations per second (pairs x
+thresholds / s), in G pairs/s.
+
+Multi-GPU (torchrun, one process per GPU): every rank filters its own shard of
+the same size (weak scaling, no collective on the data path); time = max over
+ranks of the device time; an NCCL all-reduce of the accepted-pair totals runs
+after the timed region only.
+
+--impl reference: the CPU oracle (oracle/), as it stands, timed on this host's
+cores on a bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n_pairs per GPU, read length, e values, BASELINE configs index)
+    "c2": (30_000_000, 100, list(range(0, 11)), 1),
+    "c3": (30_000_000, 150, list(range(0, 16)), 2),
+    "c4": (30_000_000, 250, list(range(0, 26)), 3),
+}
+BASE_SEED = 2103149780
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    p.add_argument("--path", default="packed", choices=["fused", "packed"])
+    p.add_argument("--n", type=int, default=None, help="override pairs per GPU")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=None)
+    return p.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/gk_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def cpu_baseline(cfg_name, sample_pairs=None, budget_s=15.0):
+    """The oracle, as it stands, on this host's cores over a bounded sample."""
+    import oracle
+    import pairgen
+    n_full, L, es, _ = CONFIGS[cfg_name]
+    cores = os.cpu_count() or 1
+    sample = sample_pairs
+    if sample is None:
+        # calibrate: ~budget_s of CPU work over the e sweep
+        probe = 2000
+        r, f = pairgen.gen_pairs(probe, L)
+        t0 = time.perf_counter()
+        for e in es:
+            oracle.filter(r, f, e, nthreads=cores)
+        dt = time.perf_counter() - t0
+        sample = int(max(1024, min(n_full, probe * budget_s / max(dt, 1e-6))))
+    r, f = pairgen.gen_pairs(sample, L)
+    t0 = time.perf_counter()
+    for e in es:
+        oracle.filter(r, f, e, nthreads=cores)
+    dt = time.perf_counter() - t0
+    value = sample * len(es) / dt / 1e9
+    return {"value": value, "unit": "Gpairs/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {sample} pairs of the {n_full}-pair {L} bp batch, e = {es[0]}..{es[-1]}, "
+                      f"{dt:.1f} s wall on {cores} threads"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_full, L, es, cidx = CONFIGS[args.config]
+    import oracle
+    import pairgen
+    cores = os.cpu_count() or 1
+    # bounded sample per step so that warmup + steps end within a few minutes
+    probe = 2000
+    r, f = pairgen.gen_pairs(probe, L)
+    t0 = time.perf_counter()
+    for e in es:
+        oracle.filter(r, f, e, nthreads=cores)
+    per_pair = (time.perf_counter() - t0) / probe
+    total_steps = args.steps + args.warmup
+    sample = int(max(1024, min(n_full, 120.0 / total_steps / max(per_pair, 1e-9))))
+    r, f = pairgen.gen_pairs(sample, L)
+    for _ in range(args.warmup):
+        for e in es:
+            oracle.filter(r, f, e, nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for e in es:
+            oracle.filter(r, f, e, nthreads=cores)
+    dt = time.perf_counter() - t0
+    value = sample * len(es) * args.steps / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "filtered pairs/sec (Gpairs/s)", "value": value,
+        "unit": "Gpairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1000 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {n_full} pairs x {L} bp, e {es[0]}..{es[-1]} "
+                               f"(BASELINE configs[{cidx}]); each step a {sample}-pair sample",
+                   "read_len": L, "e": f"{es[0]}-{es[-1]}", "profile": "paper", "seed": BASE_SEED},
+        "cpu_baseline": {"value": value, "unit": "Gpairs/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{sample} pairs per step x {len(es)} thresholds"},
+        "e2e": {"value": value, "unit": "Gpairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import pairgen
+    import paper_2103_14978_b200 as gk
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    gk.load_library()
+
+    n_cfg, L, es, cidx = CONFIGS[args.config]
+    n = args.n or n_cfg
+    # this rank's shard: pairs [rank*n, (rank+1)*n) of the seeded stream
+    reads, refs = pairgen.gen_pairs_cuda(n, L, idx0=rank * n, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    accept = torch.empty(gk.result_words(n), dtype=torch.int32, device=dev)
+    errc = torch.empty(n, dtype=torch.uint8, device=dev)
+    idx = torch.empty(n, dtype=torch.int32, device=dev)
+    n_acc = torch.zeros(len(es), dtype=torch.int64, device=dev)
+    ws = torch.empty(gk.compact_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    if args.path == "packed":
+        pq = torch.empty(gk.packed_words(n, L), dtype=torch.int32, device=dev)
+        pr = torch.empty_like(pq)
+        uq = torch.empty(gk.undef_words(n), dtype=torch.int32, device=dev)
+        ur = torch.empty_like(uq)
+    torch.cuda.synchronize(dev)
+
+    n_ev = len(es)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_ev)]
+    ev_enc = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    enc_launches = 0
+    if args.path == "packed":
+        enc_launches = 2 * (1 + (1 if n % 128 else 0) + (1 if (n + 1023) // 1024 * 32 > (n + 31) // 32 else 0))
+    launches_per_step = len(es) * 3 + enc_launches
+
+    def step(record=False):
+        if args.path == "packed":
+            if record:
+                ev_enc[0].record(stream)
+            gk.encode(reads, L, out=(pq, uq), stream=stream)
+            gk.encode(refs, L, out=(pr, ur), stream=stream)
+            if record:
+                ev_enc[1].record(stream)
+        for j, e in enumerate(es):
+            if record:
+                ev[j][0].record(stream)
+            if args.path == "fused":
+                gk.filter_ascii(reads, refs, e, L, accept=accept, errcount=errc, stream=stream)
+            else:
+                gk.filter(pq, pr, uq, ur, n, L, e, accept=accept, errcount=errc, stream=stream)
+            if record:
+                ev[j][1].record(stream)
+            gk.compact(accept, n, idx=idx, n_acc=n_acc[j:j + 1], workspace=ws, stream=stream)
+            if record:
+                ev[j][2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(dev.index)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    time.sleep(0.3)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    filt_ms = [0.0] * n_ev
+    comp_ms = [0.0] * n_ev
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    # kernel times of the LAST step's launches (events are reused each step)
+    for j in range(n_ev):
+        filt_ms[j] = ev[j][0].elapsed_time(ev[j][1])
+        comp_ms[j] = ev[j][1].elapsed_time(ev[j][2])
+    elapsed = t_start.elapsed_time(t_end)
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        tot = n_acc.clone()
+        dist.all_reduce(tot)
+        n_acc_tot = tot.cpu().tolist()
+    else:
+        n_acc_tot = n_acc.cpu().tolist()
+    if world > 1:
+        dist.barrier()
+
+    ms_per_step = elapsed / args.steps
+    filtrations = n * len(es) * world
+    value = filtrations / (ms_per_step / 1e3) / 1e9
+
+    peaks, peak_src = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 64 * clk_mhz * 1e6 / 1e12  # T int-ops/s: 148 SMs x 4 SMSPs x 16 ALU lanes
+    enc_ms = ev_enc[0].elapsed_time(ev_enc[1]) if args.path == "packed" else 0.0
+
+    def alg_ops(e):
+        # method-minimum integer ops per pair on bit-sliced words:
+        # 5 LOP3 per (position, mask) cell + 8 per position for two window counters
+        cells = L * (2 * e + 1) - e * (e + 1)
+        return (5 * cells + 8 * L) / 32.0
+
+    if args.path == "fused":
+        bytes_launch = n * (2 * L) + n / 8 + n
+        kname = "gk_filter_ascii (filter_ascii_kernel)"
+    else:
+        bytes_launch = n * (L / 2) + n / 8 + n
+        kname = "gk_filter (filter_sp_kernel<E> / filter_generic_kernel)"
+    tot_ms = sum(filt_ms)
+    hbm_ach = bytes_launch * n_ev / (tot_ms / 1e3) / 1e9
+    alu_ach = sum(n * alg_ops(e) for e in es) / (tot_ms / 1e3) / 1e12
+    if args.path == "fused":
+        roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(hbm_ach / hbm_peak, 4)}
+    elif alu_ach / alu_peak >= hbm_ach / hbm_peak:
+        roof = {"bound": "alu", "achieved": round(alu_ach, 3), "peak": round(alu_peak, 3),
+                "unit": "T int-ops/s", "frac": round(alu_ach / alu_peak, 4)}
+    else:
+        roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(hbm_ach / hbm_peak, 4)}
+    roof.update({"kernel": kname, "traffic": None, "peak_source": peak_src,
+                 "alu_peak_basis": f"148 SM x 64 ALU lanes/clk x {clk_mhz:.0f} MHz (B200_PROFILING.md / B300_MICROARCH.md)",
+                 "hbm_frac": round(hbm_ach / hbm_peak, 4), "alu_frac": round(alu_ach / alu_peak, 4),
+                 "bytes_per_launch": bytes_launch, "mean_launch_ms": round(tot_ms / n_ev, 4),
+                 "share_of_step": round(tot_ms / ms_per_step, 4)})
+    per_e = {}
+    for j, e in enumerate(es):
+        t = filt_ms[j] / 1e3
+        per_e[str(e)] = {"filter_ms": round(filt_ms[j], 4), "compact_ms": round(comp_ms[j], 4),
+                         "Gpairs_s_filter": round(n / t / 1e9, 3),
+                         "hbm_frac": round(bytes_launch / t / 1e9 / hbm_peak, 4),
+                         "alu_frac": round(n * alg_ops(e) / t / 1e12 / alu_peak, 4),
+                         "accepted": int(n_acc_tot[j])}
+    encode = None
+    if args.path == "packed":
+        enc_bytes = 2 * (n * L + n * L / 4 + n / 8)
+        encode = {"ms": round(enc_ms, 4), "GB_s": round(enc_bytes / (enc_ms / 1e3) / 1e9, 1),
+                  "hbm_frac": round(enc_bytes / (enc_ms / 1e3) / 1e9 / hbm_peak, 4),
+                  "bytes": enc_bytes, "share_of_step": round(enc_ms / ms_per_step, 4)}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(gk, torch, dev, n, L, es, rank, world, args)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, args.cpu_sample)
+
+    if rank == 0:
+        line = {
+            "metric": "filtered pairs/sec (Gpairs/s)",
+            "value": round(value, 4), "unit": "Gpairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {
+                "workload": f"{args.config}: {n} pairs x {L} bp per GPU, e swept {es[0]}..{es[-1]} "
+                            f"(BASELINE configs[{cidx}]); step = per e: a1-a6 + a7",
+                "n_pairs_per_gpu": n, "read_len": L, "e": f"{es[0]}-{es[-1]}",
+                "path": "gk_filter_ascii + gk_compact" if args.path == "fused"
+                        else "gk_encode x2 + gk_filter + gk_compact",
+                "profile": "paper", "seed": BASE_SEED,
+                "l2": f"inputs {2 * n * L / 1e9:.1f} GB per GPU > 126 MB L2 (no flush needed)",
+                "parallelism": f"dp{world} (pairs sharded, no data-path collective)"},
+            "roofline": roof,
+            "encode": encode,
+            "per_e": per_e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_e2e(gk, torch, dev, n, L, es, rank, world, args):
+    """Same metric through the public host-buffer API (gk_filter_host): every
+    step copies the batch host->device and the results device->host, per e."""
+    import pairgen
+    n_e2e = n
+    # host copies of this rank's shard (pinned)
+    r_h, f_h = pairgen.gen_pairs_cuda(n_e2e, L, idx0=rank * n, device=dev)
+    hr = torch.empty((n_e2e, L), dtype=torch.uint8, pin_memory=True)
+    hf = torch.empty((n_e2e, L), dtype=torch.uint8, pin_memory=True)
+    hr.copy_(r_h)
+    hf.copy_(f_h)
+    del r_h, f_h
+    acc = torch.empty(gk.result_words(n_e2e), dtype=torch.int32, pin_memory=True)
+    err = torch.empty(n_e2e, dtype=torch.uint8, pin_memory=True)
+    chunk = 1 << 21
+    ws = torch.empty(gk.host_workspace_bytes(chunk, L), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize(dev)
+
+    def one():
+        for e in es:
+            gk.filter_host(hr, hf, e, L, accept=acc, errcount=err, workspace=ws, chunk_pairs=chunk)
+
+    one()  # warm-up
+    steps = max(1, min(args.steps, 2))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = (time.perf_counter() - t0) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    value = n_e2e * len(es) * world / dt / 1e9
+    return {"value": round(value, 4), "unit": "Gpairs/s",
+            "h2d_bytes_per_step": 2 * n_e2e * L * len(es),
+            "d2h_bytes_per_step": (n_e2e // 8 + n_e2e) * len(es),
+            "api": "gk_filter_host (pinned host buffers, 2-stream chunked pipeline)",
+            "n_pairs_per_gpu": n_e2e, "timer": "host wall clock around the synchronous call"}
+
+
+if __name__ == "__main__":
+    main()

@@ -10,7 +10,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libgk.so")
 SOURCES = ["gk_api.cu", "gk_encode.cu", "gk_filter.cu", "gk_filter_ascii.cu", "gk_compact.cu"]
-HEADERS = ["gk_common.cuh", "gk_kernels.cuh", "gk_encode_core.cuh", "gk_filter_core.cuh"]
+HEADERS = ["gk_common.cuh", "gk_kernels.cuh", "gk_encode_core.cuh", "gk_filter_core.cuh",
+           "gk_tma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -68,48 +68,54 @@ __global__ void __launch_bounds__(CP_THREADS) compact_count_kernel(const uint32_
 __global__ void __launch_bounds__(CP_THREADS) compact_write_kernel(
     const uint32_t* __restrict__ bits, int64_t n, const uint32_t* __restrict__ cta_counts,
     uint32_t* __restrict__ idx, unsigned long long* __restrict__ n_acc) {
+  // CTA: 8 warps x 256 consecutive words.  Warp offsets come from a block scan of
+  // the warps' popcounts; inside a warp the words are visited in order and lane j
+  // writes the index of bit j, so each word's accepted pairs are one contiguous,
+  // coalesced run of indices.
   __shared__ uint32_t sm[CP_THREADS / 32];
+  __shared__ unsigned long long sm_part[CP_THREADS / 32];
   __shared__ unsigned long long sm_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nwords = (n + 31) / 32;
-  // global offset of this CTA: sum of the totals of all previous CTAs
   unsigned long long part = 0ull;
   for (unsigned b = threadIdx.x; b < blockIdx.x; b += CP_THREADS) part += cta_counts[b];
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) part += __shfl_down_sync(0xFFFFFFFFu, part, d);
-  __shared__ unsigned long long sm_part[CP_THREADS / 32];
-  if ((threadIdx.x & 31) == 0) sm_part[threadIdx.x >> 5] = part;
+  if (lane == 0) sm_part[warp] = part;
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long s = 0ull;
     for (int w = 0; w < CP_THREADS / 32; ++w) s += sm_part[w];
     sm_base = s;
   }
-  // each thread owns CP_WORDS_PER_THREAD consecutive words (ascending order)
-  const int64_t w0 = (int64_t)blockIdx.x * CP_WORDS_PER_CTA + (int64_t)threadIdx.x * CP_WORDS_PER_THREAD;
+  const int64_t wbase = (int64_t)blockIdx.x * CP_WORDS_PER_CTA + (int64_t)warp * 256;
   uint32_t words[CP_WORDS_PER_THREAD];
   uint32_t c = 0u;
 #pragma unroll
   for (int t = 0; t < CP_WORDS_PER_THREAD; ++t) {
-    words[t] = load_word(bits, w0 + t, nwords, n);
+    words[t] = load_word(bits, wbase + 32 * t + lane, nwords, n);
     c += __popc(words[t]);
   }
   uint32_t total;
-  const uint32_t off = block_exclusive_scan(c, sm, total);
-  const unsigned long long base = sm_base;
+  const uint32_t before = block_exclusive_scan(c, sm, total);  // lanes of warp w before lane
+  // warp start offset = exclusive prefix of lane 0 of this warp
+  const uint32_t warp_off = __shfl_sync(0xFFFFFFFFu, before, 0);
+  unsigned long long o = sm_base + warp_off;
   if (idx != nullptr) {
-    unsigned long long o = base + off;
+    const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int t = 0; t < CP_WORDS_PER_THREAD; ++t) {
-      uint32_t v = words[t];
-      const uint32_t pbase = (uint32_t)((w0 + t) * 32);
-      while (v) {
-        const int b = __ffs(v) - 1;
-        idx[o++] = pbase + (uint32_t)b;
-        v &= v - 1u;
+#pragma unroll 4
+      for (int src = 0; src < 32; ++src) {
+        const uint32_t v = __shfl_sync(0xFFFFFFFFu, words[t], src);
+        if (v == 0u) continue;
+        if ((v >> lane) & 1u)
+          idx[o + __popc(v & lt)] = (uint32_t)((wbase + 32 * t + src) * 32 + lane);
+        o += __popc(v);
       }
     }
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *n_acc = base + total;
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *n_acc = sm_base + total;
 }
 
 size_t compact_workspace_bytes(int64_t n) {

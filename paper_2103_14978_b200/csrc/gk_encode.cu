@@ -20,18 +20,24 @@
 #include "gk_common.cuh"
 #include "gk_encode_core.cuh"
 #include "gk_kernels.cuh"
+#include "gk_tma.cuh"
+
+#ifndef GK_ENCODE_TMA
+#define GK_ENCODE_TMA 1
+#endif
 
 namespace gk {
 
+// Generic encoder: any alignment / stride / tail; also the tail of the TMA path.
 template <bool ALIGNED>
 __global__ void __launch_bounds__(128) encode_kernel(const uint8_t* __restrict__ seqs,
                                                      int64_t n, int len, int64_t stride,
                                                      uint32_t* __restrict__ packed,
                                                      uint32_t* __restrict__ undef,
-                                                     int groups_per_cta) {
+                                                     int groups_per_cta, int64_t first_group) {
   extern __shared__ __align__(16) uint8_t sm_enc[];
   const int64_t ngroups = (n + 31) / 32;
-  const int64_t g0 = (int64_t)blockIdx.x * groups_per_cta;
+  const int64_t g0 = first_group + (int64_t)blockIdx.x * groups_per_cta;
   const int64_t s0 = g0 * 32;
   int64_t s1 = s0 + (int64_t)groups_per_cta * 32;
   if (s1 > n) s1 = n;
@@ -71,9 +77,113 @@ __global__ void encode_tail_kernel(int64_t first_group, int64_t end_group, int l
   }
 }
 
-int launch_encode(const uint8_t* seqs, int64_t n, int len, int64_t stride, uint32_t* packed,
-                  uint32_t* undef, cudaStream_t stream) {
-  const int64_t ngroups = (n + 31) / 32;
+// TMA encoder: full blocks of 4 groups (128 sequences).  Persistent CTAs of 4
+// warps; warp w encodes group 4b+w of block b.  Its 32 rows (one contiguous span
+// of 32*stride bytes) arrive by one cp.async.bulk into a double buffer, the next
+// block's span being prefetched while the current one is encoded.  The 4 groups'
+// words are collected in shared memory and written out as full 32-byte sectors.
+template <int PMAX, int SM4, bool LPART>
+__global__ void __launch_bounds__(128) encode_tma_kernel(const uint8_t* __restrict__ seqs,
+                                                         int64_t nblocks, int len, int stride,
+                                                         uint32_t* __restrict__ packed,
+                                                         uint32_t* __restrict__ undef) {
+  constexpr int NIT = PMAX / 128;          // quad iterations per lane (4 bytes x 32 lanes)
+  constexpr uint32_t BUF = 32u * PMAX;     // bytes of one staging buffer
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* stage = sm + (size_t)warp * 2 * BUF;                    // [2][32*PMAX]
+  const int nq = (len + 3) >> 2;
+  uint2* outt = reinterpret_cast<uint2*>(sm + 4 * 2 * BUF);        // [4 warps][4 m][nq]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 4 * 2 * BUF + (size_t)16 * 8 * nq);
+  uint64_t* mybar = bars + 2 * warp;
+  if (lane == 0) {
+    mbar_init(&mybar[0], 1);
+    mbar_init(&mybar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  RowAddr<SM4> ra;
+  ra.init(smem_u32(stage), (uint32_t)stride, lane);
+  const uint32_t span = 32u * (uint32_t)stride;
+
+  int64_t b = blockIdx.x;
+  if (b >= nblocks) return;
+  if (lane == 0) {
+    mbar_arrive_expect_tx(&mybar[0], span);
+    tma_load_1d(stage, seqs + (4 * b + warp) * (int64_t)span, span, &mybar[0]);
+  }
+  uint32_t phase[2] = {0u, 0u};
+  for (int i = 0; b < nblocks; ++i, b += gridDim.x) {
+    const int buf = i & 1;
+    const int64_t bn = b + gridDim.x;
+    if (lane == 0 && bn < nblocks) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&mybar[buf ^ 1], span);
+      tma_load_1d(stage + (buf ^ 1) * BUF, seqs + (4 * bn + warp) * (int64_t)span, span,
+                  &mybar[buf ^ 1]);
+    }
+    mbar_wait(&mybar[buf], phase[buf]);
+    phase[buf] ^= 1u;
+    const int64_t g = 4 * b + warp;
+    uint2* myout = outt + (size_t)warp * 4 * nq;
+    const uint32_t und = encode_group_v2<SM4, LPART, NIT>(
+        ra, buf * BUF, len, [&](int q, int m, uint32_t hi, uint32_t lo) {
+          myout[m * nq + q] = make_uint2(hi, lo);
+        });
+    if (lane == 0) undef[g] = und;
+    __syncwarp();
+    __syncthreads();
+    // write the 4 groups' words: per position 32 contiguous bytes
+    const int64_t tile = (4 * b) >> 5;
+    const int gl0 = (int)((4 * b) & 31);
+    uint2* dst = reinterpret_cast<uint2*>(packed);
+    for (int t = threadIdx.x; t < 4 * len; t += 128) {
+      const int pos = t >> 2, w = t & 3;
+      dst[((tile * len + pos) * 32 + gl0 + w)] = outt[((size_t)w * 4 + (pos & 3)) * nq + (pos >> 2)];
+    }
+    __syncthreads();
+  }
+}
+
+template <int PMAX, int SM4, bool LPART>
+static void launch_tma(const uint8_t* seqs, int64_t nblocks, int len, int stride,
+                       uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
+  const int nq = (len + 3) >> 2;
+  const size_t smem = (size_t)4 * 2 * 32 * PMAX + (size_t)16 * 8 * nq + 64;
+  auto kern = encode_tma_kernel<PMAX, SM4, LPART>;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > nblocks) grid = nblocks;
+  kern<<<(unsigned)grid, 128, smem, stream>>>(seqs, nblocks, len, stride, packed, undef);
+}
+
+template <int PMAX>
+static void dispatch_tma(const uint8_t* seqs, int64_t nblocks, int len, int stride,
+                         uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
+  const bool lpart = (len & 3) != 0;
+  switch (stride & 3) {
+    case 0: lpart ? launch_tma<PMAX, 0, true>(seqs, nblocks, len, stride, packed, undef, stream)
+                  : launch_tma<PMAX, 0, false>(seqs, nblocks, len, stride, packed, undef, stream); break;
+    case 1: lpart ? launch_tma<PMAX, 1, true>(seqs, nblocks, len, stride, packed, undef, stream)
+                  : launch_tma<PMAX, 1, false>(seqs, nblocks, len, stride, packed, undef, stream); break;
+    case 2: lpart ? launch_tma<PMAX, 2, true>(seqs, nblocks, len, stride, packed, undef, stream)
+                  : launch_tma<PMAX, 2, false>(seqs, nblocks, len, stride, packed, undef, stream); break;
+    default: lpart ? launch_tma<PMAX, 3, true>(seqs, nblocks, len, stride, packed, undef, stream)
+                   : launch_tma<PMAX, 3, false>(seqs, nblocks, len, stride, packed, undef, stream); break;
+  }
+}
+
+static void launch_generic(const uint8_t* seqs, int64_t n, int len, int64_t stride,
+                           uint32_t* packed, uint32_t* undef, int64_t first_group,
+                           cudaStream_t stream) {
+  const int64_t ngroups = (n + 31) / 32 - first_group;
+  if (ngroups <= 0) return;
   int gpc = (int)(49152 / (32 * stride));
   if (gpc > 4) gpc = 4;
   if (gpc < 1) gpc = 1;
@@ -88,10 +198,28 @@ int launch_encode(const uint8_t* seqs, int64_t n, int len, int64_t stride, uint3
   }
   if (aligned)
     encode_kernel<true><<<(unsigned)blocks, gpc * 32, smem, stream>>>(seqs, n, len, stride,
-                                                                      packed, undef, gpc);
+                                                                      packed, undef, gpc, first_group);
   else
     encode_kernel<false><<<(unsigned)blocks, gpc * 32, smem, stream>>>(seqs, n, len, stride,
-                                                                       packed, undef, gpc);
+                                                                       packed, undef, gpc, first_group);
+}
+
+int launch_encode(const uint8_t* seqs, int64_t n, int len, int64_t stride, uint32_t* packed,
+                  uint32_t* undef, cudaStream_t stream) {
+  const int64_t ngroups = (n + 31) / 32;
+  int64_t first_generic = 0;
+  const bool tma_ok = ((reinterpret_cast<uintptr_t>(seqs) & 15u) == 0) && stride <= 512 &&
+                      GK_ENCODE_TMA;
+  if (tma_ok) {
+    const int64_t nblocks = n / 128;  // full blocks of 4 groups
+    if (nblocks > 0) {
+      if (stride <= 128) dispatch_tma<128>(seqs, nblocks, len, (int)stride, packed, undef, stream);
+      else if (stride <= 256) dispatch_tma<256>(seqs, nblocks, len, (int)stride, packed, undef, stream);
+      else dispatch_tma<512>(seqs, nblocks, len, (int)stride, packed, undef, stream);
+    }
+    first_generic = nblocks * 4;
+  }
+  launch_generic(seqs, n, len, stride, packed, undef, first_generic, stream);
   const int64_t tile_end = ((ngroups + 31) / 32) * 32;
   if (tile_end > ngroups) {
     const int64_t total = (tile_end - ngroups) * len;

@@ -119,4 +119,117 @@ __device__ __forceinline__ uint32_t encode_group(const uint8_t* sm, uint32_t row
   return und;
 }
 
+
+// ---------------------------------------------------------------------------
+// Encoder v2 (TMA-staged): the 32 rows of a group sit in shared memory at
+// buf + s*stride (buf 16-byte aligned); lane q encodes base positions
+// 4q..4q+3 (q = lane + 32*it).  The smem address of every row at the lane's
+// first column is computed once per kernel (32 registers), so each 4-byte
+// word costs one LDS with an immediate offset (two LDS + one PRMT for rows
+// whose start is not 4-byte aligned: their misalignment (s*stride) % 4 is a
+// compile-time function of s and SM4 = stride % 4).
+template <int SM4>
+struct RowAddr {
+  uint32_t a[32];
+  __device__ __forceinline__ void init(uint32_t buf, uint32_t stride, int lane) {
+#pragma unroll
+    for (int s = 0; s < 32; ++s) a[s] = buf + (uint32_t)s * stride + 4u * lane - ((s * SM4) & 3);
+  }
+};
+
+template <int SM4, int S>
+__device__ __forceinline__ uint32_t row_word(const RowAddr<SM4>& ra, uint32_t off) {
+  constexpr int d = (S * SM4) & 3;
+  const uint32_t a = ra.a[S] + off;
+  uint32_t lo;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(lo) : "r"(a));
+  if constexpr (d == 0) {
+    return lo;
+  } else {
+    uint32_t hi;
+    asm volatile("ld.shared.b32 %0, [%1+4];" : "=r"(hi) : "r"(a));
+    return __byte_perm(lo, hi, d == 1 ? 0x4321 : (d == 2 ? 0x5432 : 0x6543));
+  }
+}
+
+// err | (w ^ canonical(w)): 0 in every byte of a valid base (see invalid_bytes).
+__device__ __forceinline__ uint32_t acc_invalid(uint32_t bad, uint32_t w) {
+  const uint32_t base = (w & 0x26262626u) | 0x41414141u;
+  const uint32_t tflag = __umulhi(w, 1u << 30) & ~__umulhi(w, 1u << 31) & 0x01010101u;
+  const uint32_t m = tflag * 15u + base;
+  return bad | (w ^ m);
+}
+
+template <int SM4, int BLK, bool LPART>
+__device__ __forceinline__ void encode_block(const RowAddr<SM4>& ra, uint32_t off,
+                                             const bool (&pm)[4], uint32_t& bad,
+                                             uint32_t (&hb)[4], uint32_t (&lb)[4]) {
+  const uint32_t w0 = row_word<SM4, 4 * BLK + 0>(ra, off);
+  const uint32_t w1 = row_word<SM4, 4 * BLK + 1>(ra, off);
+  const uint32_t w2 = row_word<SM4, 4 * BLK + 2>(ra, off);
+  const uint32_t w3 = row_word<SM4, 4 * BLK + 3>(ra, off);
+  const uint32_t t0 = __byte_perm(w0, w1, 0x5140);
+  const uint32_t t1 = __byte_perm(w0, w1, 0x7362);
+  const uint32_t t2 = __byte_perm(w2, w3, 0x5140);
+  const uint32_t t3 = __byte_perm(w2, w3, 0x7362);
+  uint32_t r[4];
+  r[0] = __byte_perm(t0, t2, 0x5410);
+  r[1] = __byte_perm(t0, t2, 0x7632);
+  r[2] = __byte_perm(t1, t3, 0x5410);
+  r[3] = __byte_perm(t1, t3, 0x7632);
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    uint32_t x = r[m];
+    if (LPART) x = pm[m] ? x : 0x41414141u;  // positions >= len of the last quad
+    bad = acc_invalid(bad, x);
+    hb[m] = __funnelshift_l(gather_bit2(x), hb[m], 4);          // ALU pipe
+    lb[m] = lb[m] * 16u + __umulhi(gather_bit1(x), 16u);        // FMA pipe
+  }
+}
+
+// Encode all quads of the lane for the staged group at buffer offset `boff`.
+// emit(q, m, hi_plane, lo_plane) for every position 4q+m < len.
+template <int SM4, bool LPART, int NIT, typename Emit>
+__device__ __forceinline__ uint32_t encode_group_v2(const RowAddr<SM4>& ra, uint32_t boff,
+                                                    int len, Emit&& emit) {
+  const int lane = threadIdx.x & 31;
+  const int nquads = (len + 3) >> 2;
+  uint32_t bad[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) bad[b] = 0u;
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int q = lane + 32 * it;
+    if (q < nquads) {
+      const int rem = len - 4 * q;
+      bool pm[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) pm[m] = m < rem;
+      uint32_t hb[4] = {0u, 0u, 0u, 0u}, lb[4] = {0u, 0u, 0u, 0u};
+      const uint32_t off = boff + 128u * it;
+      encode_block<SM4, 7, LPART>(ra, off, pm, bad[7], hb, lb);
+      encode_block<SM4, 6, LPART>(ra, off, pm, bad[6], hb, lb);
+      encode_block<SM4, 5, LPART>(ra, off, pm, bad[5], hb, lb);
+      encode_block<SM4, 4, LPART>(ra, off, pm, bad[4], hb, lb);
+      encode_block<SM4, 3, LPART>(ra, off, pm, bad[3], hb, lb);
+      encode_block<SM4, 2, LPART>(ra, off, pm, bad[2], hb, lb);
+      encode_block<SM4, 1, LPART>(ra, off, pm, bad[1], hb, lb);
+      encode_block<SM4, 0, LPART>(ra, off, pm, bad[0], hb, lb);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        if (m < rem) emit(q, m, hb[m], hb[m] ^ lb[m]);  // paper code: high = b2, low = b1^b2
+    }
+  }
+  uint32_t und = 0u;
+#pragma unroll
+  for (int blk = 0; blk < 8; ++blk) {
+    const uint32_t b = __reduce_or_sync(0xFFFFFFFFu, bad[blk]);
+    // byte k != 0 -> bit 4*blk+k
+    const uint32_t nz = ((b & 0x7F7F7F7Fu) + 0x7F7F7F7Fu | b) & 0x80808080u;
+    und |= ((nz >> 7) & 1u) << (4 * blk) | ((nz >> 15) & 1u) << (4 * blk + 1) |
+           ((nz >> 23) & 1u) << (4 * blk + 2) | ((nz >> 31) & 1u) << (4 * blk + 3);
+  }
+  return und;
+}
+
 }  // namespace gk

@@ -16,6 +16,10 @@
 #include "gk_filter_core.cuh"
 #include "gk_kernels.cuh"
 
+#ifndef GK_FILTER_RING
+#define GK_FILTER_RING 1
+#endif
+
 namespace gk {
 
 template <int E>
@@ -26,18 +30,44 @@ __global__ void __launch_bounds__(128) filter_sp_kernel(
   const int lane = threadIdx.x & 31;
   const int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t g = tile * 32 + lane;
-  if (g * 32 >= n) return;
+  if (tile * 1024 >= n) return;  // whole warp leaves together (warp-level TMA ring)
+#if GK_FILTER_RING
+  extern __shared__ __align__(128) uint8_t sm_ring[];
+  const int warp = threadIdx.x >> 5;
+  uint8_t* mine = sm_ring + (size_t)warp * (2 * 4 * 8 * 32 * 8 + 64);
+  RingSrc src;
+  src.gq = reads + tile * (int64_t)len * 32;
+  src.gr = refs + tile * (int64_t)len * 32;
+  src.sq = reinterpret_cast<uint2*>(mine);
+  src.sr = src.sq + 4 * 8 * 32;
+  src.bq = reinterpret_cast<uint64_t*>(mine + 2 * 4 * 8 * 32 * 8);
+  src.br = src.bq + 4;
+  src.len = len;
+  src.nblk = (len + 7) >> 3;
+  src.lane = lane;
+  if (lane == 0) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      mbar_init(&src.bq[b], 1);
+      mbar_init(&src.br[b], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncwarp();
+  src.start();
+#else
   GlobalGroupSrc src;
   src.q = reads + tile * (int64_t)len * 32 + lane;
   src.r = refs + tile * (int64_t)len * 32 + lane;
   src.len = len;
+#endif
 
   SinglePass<E> sp;
-  run_range<E>(sp, src, len, 0, len);
+  run_range<E, true>(sp, src, len, 0, len);
   uint32_t cA[8], cF[8];
   sp.cA.planes(cA);
   sp.cF.planes(cF);
-  finish_group(cA, cF, E, __ldg(rund + g) | __ldg(fund + g), g, n, accept, errc);
+  if (g * 32 < n) finish_group(cA, cF, E, __ldg(rund + g) | __ldg(fund + g), g, n, accept, errc);
 }
 
 // ---------------------------------------------------------------------------
@@ -69,8 +99,12 @@ static void launch_sp(const uint2* reads, const uint2* refs, const uint32_t* run
   const int64_t tiles = (n + 1023) / 1024;
   const int warps = 4;
   const int64_t blocks = (tiles + warps - 1) / warps;
-  filter_sp_kernel<E><<<(unsigned)blocks, warps * 32, 0, stream>>>(reads, refs, rund, fund, n,
-                                                                    len, accept, errc);
+  const size_t smem = GK_FILTER_RING ? (size_t)warps * (2 * 4 * 8 * 32 * 8 + 64) : 0;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(filter_sp_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  filter_sp_kernel<E><<<(unsigned)blocks, warps * 32, smem, stream>>>(reads, refs, rund, fund, n,
+                                                                       len, accept, errc);
 }
 
 template <int E>

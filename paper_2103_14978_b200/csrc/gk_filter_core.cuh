@@ -25,6 +25,7 @@
 // Per position and mask: 2 LOP3 (mismatch) + 3 LOP3 (amend + AND).
 #pragma once
 #include "gk_common.cuh"
+#include "gk_tma.cuh"
 
 namespace gk {
 
@@ -84,6 +85,7 @@ struct CsaCounter {
 // Read source: words of the thread's group at base position `pos`; (0,0) outside
 // [0, len).  x = plane 0 (high bit), y = plane 1 (low bit).
 struct GlobalGroupSrc {
+  static constexpr bool kHoistLoads = true;
   const uint2* q;  // read  words of (tile, lane) at position 0; stride 32 uint2 per position
   const uint2* r;  // reference words
   int len;
@@ -106,9 +108,9 @@ struct SinglePass {
   uint32_t fprev, aprev;
   CsaCounter cF, cA;
 
-  __host__ __device__ __forceinline__ static int mask_k(int m) { return (m + 1) >> 1; }
-  __host__ __device__ __forceinline__ static bool mask_is_d(int m) { return (m & 1) != 0; }
-  __host__ __device__ __forceinline__ static int mask_q(int m) {
+  __host__ __device__ __forceinline__ static constexpr int mask_k(int m) { return (m + 1) >> 1; }
+  __host__ __device__ __forceinline__ static constexpr bool mask_is_d(int m) { return (m & 1) != 0; }
+  __host__ __device__ __forceinline__ static constexpr int mask_q(int m) {
     return m == 0 ? E : (mask_is_d(m) ? E - mask_k(m) : E + mask_k(m));
   }
 
@@ -139,29 +141,30 @@ struct SinglePass {
     ql[QW - 1] = qn.y;
   }
 
-  // Raw mask words at position p (newest), with vacancy / range checks if CHECK.
-  template <bool CHECK>
-  __host__ __device__ __forceinline__ void mismatch_all(int p, int len, uint2 rn, uint32_t (&xn)[NM]) const {
+  // Raw mask words at position p (the newest).  CD: check the start side
+  // (p >= 0, deletion vacancy p - k >= 0); CL: check the end side (p < len,
+  // insertion vacancy p + k < len).  With a compile-time p (unrolled head) or
+  // p = len - c (unrolled tail) these checks fold away.
+  template <bool CD, bool CL>
+  __host__ __device__ __forceinline__ void mismatch_all(int p, int len, uint2 rn,
+                                                       uint32_t (&xn)[NM]) const {
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
       const int j = mask_q(m);
       uint32_t v = mismatch(rn.x, rn.y, qh[j], ql[j]);
-      if (CHECK) {
-        const int k = mask_k(m);
-        bool ok = (p >= 0) && (p < len);
-        if (m != 0) ok = ok && (mask_is_d(m) ? (p - k >= 0) : (p + k < len));
-        v = ok ? v : 0u;
-      }
-      xn[m] = v;
+      bool ok = true;
+      if (CD) ok = ok && (p >= 0) && (m == 0 || !mask_is_d(m) || p - mask_k(m) >= 0);
+      if (CL) ok = ok && (p < len) && (m == 0 || mask_is_d(m) || p + mask_k(m) < len);
+      xn[m] = ok ? v : 0u;
     }
   }
 
   // Priming step: only make x at p = i+2 the newest value (no finalize).
-  template <bool CHECK>
+  template <bool CD, bool CL>
   __host__ __device__ __forceinline__ void prime(int i, int len, uint2 qn, uint2 rn) {
     push_q(qn);
     uint32_t xn[NM];
-    mismatch_all<CHECK>(i + 2, len, rn, xn);
+    mismatch_all<CD, CL>(i + 2, len, rn, xn);
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
       x[m][0] = x[m][1];
@@ -172,22 +175,21 @@ struct SinglePass {
   }
 
   // Full step: x at p = i+2 becomes newest; position i is finalized.
+  // notstart = ~0 unless i is the first base of a 4-base window (R7).
   // Returns the F and A0 run-start words of position i.
-  template <bool CHECK>
-  __host__ __device__ __forceinline__ void step(int i, int len, uint2 qn, uint2 rn, uint32_t& sF,
-                                       uint32_t& sA) {
+  template <bool CD, bool CL>
+  __host__ __device__ __forceinline__ void step(int i, int len, uint2 qn, uint2 rn,
+                                                uint32_t notstart, uint32_t& sF, uint32_t& sA) {
     push_q(qn);
     uint32_t xn[NM];
-    mismatch_all<CHECK>(i + 2, len, rn, xn);
+    mismatch_all<CD, CL>(i + 2, len, rn, xn);
     uint32_t F = 0xFFFFFFFFu, A0 = 0u;
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
       const uint32_t a = amend(x[m][0], x[m][1], x[m][2], x[m][3], xn[m]);
-      bool apply = true;
-      if (CHECK && m != 0) {
-        const int k = mask_k(m);
-        apply = mask_is_d(m) ? (i >= k) : (i < len - k);
-      }
+      bool apply = true;  // edge fix: vacated positions are 1 after amendment (:109)
+      if (CD && m != 0 && mask_is_d(m)) apply = i >= mask_k(m);
+      if (CL && m != 0 && !mask_is_d(m)) apply = i < len - mask_k(m);
       if (m == 0) A0 = a;
       if (apply) F &= a;
       x[m][0] = x[m][1];
@@ -195,8 +197,6 @@ struct SinglePass {
       x[m][2] = x[m][3];
       x[m][3] = xn[m];
     }
-    // positions i >= len carry no errors (R13); windows start at multiples of 4 (R7)
-    const uint32_t notstart = (i & 3) ? 0xFFFFFFFFu : 0u;
     sF = F & ~(fprev & notstart);
     sA = A0 & ~(aprev & notstart);
     fprev = F;
@@ -204,56 +204,115 @@ struct SinglePass {
   }
 };
 
+__host__ __device__ __forceinline__ uint32_t notstart_of(int i) {
+  return (i & 3) ? 0xFFFFFFFFu : 0u;
+}
+
 // Filter base positions [lo, hi) of the thread's group (lo % 4 == 0, so the
 // counts of disjoint ranges add up: windows never straddle a range border).
-// Positions where some mask is vacated or out of range run checked steps;
-// the interior [max(lo,E), len-E-2) runs unchecked, unrolled by 8, with a
-// static carry-save tree for the two counters.
-template <int E, class Src>
-__host__ __device__ __forceinline__ void run_range(SinglePass<E>& sp, const Src& src, int len, int lo,
-                                          int hi) {
-  sp.init(src, lo - 2);
+//   * a range that starts at 0 runs a fully unrolled head [0, H) (H = E rounded
+//     up to 8) in which every vacancy check of the deletion masks is a
+//     compile-time constant;
+//   * a range that ends at len runs a fully unrolled tail [len-E-2, len) whose
+//     insertion-side checks are constants relative to len;
+//   * the rest runs unchecked steps, 8 per iteration with a static carry-save
+//     count tree, then up to 7 single steps.
+// Short reads (or ranges that violate those assumptions) take checked steps.
+template <int E, bool FULL = false, class Src>
+__host__ __device__ __forceinline__ void run_range(SinglePass<E>& sp, const Src& src, int len,
+                                                   int lo, int hi) {
+  constexpr int H = ((E + 7) / 8) * 8;
+  constexpr int T = E + 2;
+  const bool head = FULL || lo == 0, tail = FULL || hi == len;
+  const int mid_lo = head ? H : lo;
+  const int mid_hi = tail ? len - T : hi;
+  const bool fast = len >= H + T + E + 4 && mid_lo <= mid_hi && (head || lo >= E + 2) &&
+                    (tail || hi <= len - T);
+  if (!fast) {
+    sp.init(src, lo - 2);
 #pragma unroll 1
-  for (int i = lo - 4; i < lo; ++i)
-    sp.template prime<true>(i, len, src.ldq(i + 2 + E), src.ldr(i + 2));
-  int mb = lo > E ? lo : E;
-  mb = ((mb + 7) >> 3) << 3;
-  int lim = len - E - 2;
-  if (hi < lim) lim = hi;
-  int me = mb;
-  if (lim > mb) me = mb + ((lim - mb) >> 3 << 3);
-  const int head_end = me > mb ? mb : hi;
-  int i = lo;
+    for (int i = lo - 4; i < lo; ++i)
+      sp.template prime<true, true>(i, len, src.ldq(i + 2 + E), src.ldr(i + 2));
 #pragma unroll 1
-  for (; i < head_end; ++i) {
-    uint32_t sF, sA;
-    sp.template step<true>(i, len, src.ldq(i + 2 + E), src.ldr(i + 2), sF, sA);
-    sp.cF.add1(sF);
-    sp.cA.add1(sA);
+    for (int i = lo; i < hi; ++i) {
+      uint32_t sF, sA;
+      sp.template step<true, true>(i, len, src.ldq(i + 2 + E), src.ldr(i + 2), notstart_of(i), sF,
+                                   sA);
+      sp.cF.add1(sF);
+      sp.cA.add1(sA);
+    }
+    return;
   }
-  if (me > mb) {
+  sp.init(src, lo - 2);
+  if (head) {
+#pragma unroll
+    for (int i = -4; i < 0; ++i)
+      sp.template prime<true, false>(i, len, src.ldq(i + 2 + E), src.ldr(i + 2));
+#pragma unroll
+    for (int ib = 0; ib < H; ib += 8) {
+      uint32_t sF[8], sA[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = ib + u;
+        sp.template step<true, false>(i, len, src.ldq_nc(i + 2 + E), src.ldr_nc(i + 2),
+                                      notstart_of(u), sF[u], sA[u]);
+      }
+      sp.cF.add8(sF);
+      sp.cA.add8(sA);
+    }
+  } else {
 #pragma unroll 1
-    for (int ib8 = mb >> 3; ib8 < (me >> 3); ++ib8) {
-      const int ib = ib8 << 3;
+    for (int i = lo - 4; i < lo; ++i)
+      sp.template prime<false, false>(i, len, src.ldq_nc(i + 2 + E), src.ldr_nc(i + 2));
+  }
+  // unchecked middle
+  const int m4 = mid_lo >> 2;
+  const int n8 = (mid_hi - mid_lo) >> 3;
+#pragma unroll 1
+  for (int j = 0; j < n8; ++j) {
+    const int ib = FULL ? H + (j << 3) : (m4 << 2) + (j << 3);
+    uint32_t sF[8], sA[8];
+    if constexpr (Src::kHoistLoads) {
       uint2 qn[8], rn[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         qn[u] = src.ldq_nc(ib + u + 2 + E);
         rn[u] = src.ldr_nc(ib + u + 2);
       }
-      uint32_t sF[8], sA[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) sp.template step<false>(ib + u, len, qn[u], rn[u], sF[u], sA[u]);
-      sp.cF.add8(sF);
-      sp.cA.add8(sA);
+      for (int u = 0; u < 8; ++u)
+        sp.template step<false, false>(ib + u, len, qn[u], rn[u], notstart_of(u), sF[u], sA[u]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        sp.template step<false, false>(ib + u, len, src.ldq_nc(ib + u + 2 + E),
+                                       src.ldr_nc(ib + u + 2), notstart_of(u), sF[u], sA[u]);
     }
-    i = me;
+    sp.cF.add8(sF);
+    sp.cA.add8(sA);
+  }
 #pragma unroll 1
-    for (; i < hi; ++i) {
-      uint32_t sF, sA;
-      sp.template step<true>(i, len, src.ldq(i + 2 + E), src.ldr(i + 2), sF, sA);
-      sp.cF.add1(sF);
-      sp.cA.add1(sA);
+  for (int i = mid_lo + 8 * n8; i < mid_hi; ++i) {
+    uint32_t sF, sA;
+    sp.template step<false, false>(i, len, src.ldq_nc(i + 2 + E), src.ldr_nc(i + 2),
+                                   notstart_of(i), sF, sA);
+    sp.cF.add1(sF);
+    sp.cA.add1(sA);
+  }
+  if (tail) {
+    const int i0 = len - T;
+    uint32_t sF[T], sA[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int i = i0 + t;
+      sp.template step<false, true>(i, len, src.ldq(i + 2 + E), t + 2 < T ? src.ldr_nc(i + 2)
+                                                                          : make_uint2(0u, 0u),
+                                    notstart_of(i), sF[t], sA[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      sp.cF.add1(sF[t]);
+      sp.cA.add1(sA[t]);
     }
   }
 }
@@ -359,9 +418,66 @@ __device__ __forceinline__ void generic_group(const Src& src, int len, int e, ui
   cF.planes(cf);
 }
 
+// Words of the thread's group streamed through a TMA ring in shared memory.
+// Each stream (read words Q, reference words R) of the warp's tile is cut into
+// blocks of 8 base positions (8 x 32 lanes x 8 B = 2 KB, contiguous in the packed
+// layout); 4 ring slots per stream.  Blocks are loaded by cp.async.bulk with an
+// mbarrier per slot; a lane reading the first position of a block waits for it,
+// and finishing a block b releases block b-1 (long consumed) and refills its slot
+// with block b+3.  Every position of a stream is read exactly once and in order
+// (run_range guarantees this), so the block bookkeeping folds to constants in the
+// unrolled code.
+struct RingSrc {
+  static constexpr bool kHoistLoads = false;
+  const uint2* gq;  // tile base in global memory (uint2 units; position stride 32)
+  const uint2* gr;
+  uint2* sq;        // [4 slots][8 positions][32 lanes]
+  uint2* sr;
+  uint64_t* bq;     // 4 mbarriers per stream
+  uint64_t* br;
+  int len, nblk, lane;
+
+  __device__ __forceinline__ void issue(const uint2* g, uint2* s, uint64_t* bar, int b) const {
+    if (b >= nblk) return;
+    const int np = (len - 8 * b) < 8 ? (len - 8 * b) : 8;
+    const uint32_t bytes = (uint32_t)np * 256u;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&bar[b & 3], bytes);
+    tma_load_1d(s + (b & 3) * 256, g + (int64_t)b * 256, bytes, &bar[b & 3]);
+  }
+  __device__ __forceinline__ void start() const {
+    if (lane == 0) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        issue(gq, sq, bq, b);
+        issue(gr, sr, br, b);
+      }
+    }
+  }
+  __device__ __forceinline__ uint2 rd(const uint2* g, uint2* s, uint64_t* bar, int pos) const {
+    const int b = pos >> 3;
+    if ((pos & 7) == 0) mbar_wait(&bar[b & 3], (uint32_t)(b >> 2) & 1u);
+    const uint2 v = s[(b & 3) * 256 + (pos & 7) * 32 + lane];
+    if ((pos & 7) == 7 && b >= 1) {
+      __syncwarp();
+      if (lane == 0) issue(g, s, bar, b + 3);
+    }
+    return v;
+  }
+  __device__ __forceinline__ uint2 ldq(int pos) const {
+    return (pos >= 0 && pos < len) ? rd(gq, sq, bq, pos) : make_uint2(0u, 0u);
+  }
+  __device__ __forceinline__ uint2 ldr(int pos) const {
+    return (pos >= 0 && pos < len) ? rd(gr, sr, br, pos) : make_uint2(0u, 0u);
+  }
+  __device__ __forceinline__ uint2 ldq_nc(int pos) const { return rd(gq, sq, bq, pos); }
+  __device__ __forceinline__ uint2 ldr_nc(int pos) const { return rd(gr, sr, br, pos); }
+};
+
 // Words of the thread's group from a packed tile in shared memory:
 // q[pos * pstride] / r[pos * pstride] (uint2 units), 0 outside [0, len).
 struct SmemGroupSrc {
+  static constexpr bool kHoistLoads = false;
   const uint2* q;
   const uint2* r;
   int len;

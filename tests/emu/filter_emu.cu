@@ -9,6 +9,7 @@
 using namespace gk;
 
 struct HostSrc {
+  static constexpr bool kHoistLoads = true;
   const uint32_t* q;  // packed words of (tile) base; index ((pos*32)+lane)*2
   const uint32_t* r;
   int lane, len;
