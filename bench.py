@@ -189,6 +189,7 @@ def main():
 
     import pairgen
     import paper_2103_14978_b200 as gk
+    from paper_2103_14978_b200 import sharding
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -203,7 +204,8 @@ def main():
     n_cfg, L, es, cidx = CONFIGS[args.config]
     n = args.n or n_cfg
     # this rank's shard: pairs [rank*n, (rank+1)*n) of the seeded stream
-    reads, refs = pairgen.gen_pairs_cuda(n, L, idx0=rank * n, device=dev)
+    idx0, n = sharding.weak_shard(n, rank)
+    reads, refs = pairgen.gen_pairs_cuda(n, L, idx0=idx0, device=dev)
     stream = torch.cuda.current_stream(dev)
     accept = torch.empty(gk.result_words(n), dtype=torch.int32, device=dev)
     errc = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -270,16 +272,8 @@ def main():
     for j in range(n_ev):
         filt_ms[j] = ev[j][0].elapsed_time(ev[j][1])
         comp_ms[j] = ev[j][1].elapsed_time(ev[j][2])
-    elapsed = t_start.elapsed_time(t_end)
-    if world > 1:
-        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
-        tot = n_acc.clone()
-        dist.all_reduce(tot)
-        n_acc_tot = tot.cpu().tolist()
-    else:
-        n_acc_tot = n_acc.cpu().tolist()
+    elapsed = sharding.max_over_ranks(t_start.elapsed_time(t_end), device=dev)
+    n_acc_tot = sharding.sum_over_ranks(n_acc, device=dev)
     if world > 1:
         dist.barrier()
 

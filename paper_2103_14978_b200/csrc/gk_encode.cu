@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(128) encode_tma_kernel(const uint8_t* __restri
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* stage = sm + (size_t)warp * 2 * BUF;                    // [2][32*PMAX]
   const int nq = (len + 3) >> 2;
-  uint2* outt = reinterpret_cast<uint2*>(sm + 4 * 2 * BUF);        // [4 warps][4 m][nq]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 4 * 2 * BUF + (size_t)16 * 8 * nq);
+  uint2* outt0 = reinterpret_cast<uint2*>(sm + 4 * 2 * BUF);       // 2 x [4 warps][4 m][nq]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 4 * 2 * BUF + (size_t)2 * 16 * 8 * nq);
   uint64_t* mybar = bars + 2 * warp;
   if (lane == 0) {
     mbar_init(&mybar[0], 1);
@@ -125,11 +125,11 @@ __global__ void __launch_bounds__(128) encode_tma_kernel(const uint8_t* __restri
     mbar_wait(&mybar[buf], phase[buf]);
     phase[buf] ^= 1u;
     const int64_t g = 4 * b + warp;
+    uint2* outt = outt0 + (size_t)(i & 1) * 16 * nq;  // double-buffered: one barrier per block
     uint2* myout = outt + (size_t)warp * 4 * nq;
-    const uint32_t und = encode_group_v2<SM4, LPART, NIT>(
-        ra, buf * BUF, len, [&](int q, int m, uint32_t hi, uint32_t lo) {
-          myout[m * nq + q] = make_uint2(hi, lo);
-        });
+    auto emit = [&](int q, int m, uint32_t hi, uint32_t lo) { myout[m * nq + q] = make_uint2(hi, lo); };
+    const uint32_t und = buf == 0 ? encode_group_v2<SM4, LPART, NIT, 0u>(ra, len, emit)
+                                  : encode_group_v2<SM4, LPART, NIT, BUF>(ra, len, emit);
     if (lane == 0) undef[g] = und;
     __syncwarp();
     __syncthreads();
@@ -141,7 +141,6 @@ __global__ void __launch_bounds__(128) encode_tma_kernel(const uint8_t* __restri
       const int pos = t >> 2, w = t & 3;
       dst[((tile * len + pos) * 32 + gl0 + w)] = outt[((size_t)w * 4 + (pos & 3)) * nq + (pos >> 2)];
     }
-    __syncthreads();
   }
 }
 
@@ -149,7 +148,7 @@ template <int PMAX, int SM4, bool LPART>
 static void launch_tma(const uint8_t* seqs, int64_t nblocks, int len, int stride,
                        uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
   const int nq = (len + 3) >> 2;
-  const size_t smem = (size_t)4 * 2 * 32 * PMAX + (size_t)16 * 8 * nq + 64;
+  const size_t smem = (size_t)4 * 2 * 32 * PMAX + (size_t)2 * 16 * 8 * nq + 64;
   auto kern = encode_tma_kernel<PMAX, SM4, LPART>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

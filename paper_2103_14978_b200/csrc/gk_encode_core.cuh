@@ -137,37 +137,37 @@ struct RowAddr {
   }
 };
 
-template <int SM4, int S>
-__device__ __forceinline__ uint32_t row_word(const RowAddr<SM4>& ra, uint32_t off) {
+template <int SM4, int S, uint32_t OFF>
+__device__ __forceinline__ uint32_t row_word(const RowAddr<SM4>& ra) {
   constexpr int d = (S * SM4) & 3;
-  const uint32_t a = ra.a[S] + off;
   uint32_t lo;
-  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(lo) : "r"(a));
+  asm volatile("ld.shared.b32 %0, [%1+%2];" : "=r"(lo) : "r"(ra.a[S]), "n"(OFF));
   if constexpr (d == 0) {
     return lo;
   } else {
     uint32_t hi;
-    asm volatile("ld.shared.b32 %0, [%1+4];" : "=r"(hi) : "r"(a));
+    asm volatile("ld.shared.b32 %0, [%1+%2];" : "=r"(hi) : "r"(ra.a[S]), "n"(OFF + 4));
     return __byte_perm(lo, hi, d == 1 ? 0x4321 : (d == 2 ? 0x5432 : 0x6543));
   }
 }
 
 // err | (w ^ canonical(w)): 0 in every byte of a valid base (see invalid_bytes).
 __device__ __forceinline__ uint32_t acc_invalid(uint32_t bad, uint32_t w) {
-  const uint32_t base = (w & 0x26262626u) | 0x41414141u;
+  // m = canonical byte: 0x41 | (w & 0x26), +15 for T (b2 & ~b1); the two parts
+  // have disjoint bits, so one IMAD (FMA pipe) and one LOP3 build it
   const uint32_t tflag = __umulhi(w, 1u << 30) & ~__umulhi(w, 1u << 31) & 0x01010101u;
-  const uint32_t m = tflag * 15u + base;
+  const uint32_t m = (tflag * 15u + 0x41414141u) | (w & 0x26262626u);
   return bad | (w ^ m);
 }
 
-template <int SM4, int BLK, bool LPART>
-__device__ __forceinline__ void encode_block(const RowAddr<SM4>& ra, uint32_t off,
-                                             const bool (&pm)[4], uint32_t& bad,
-                                             uint32_t (&hb)[4], uint32_t (&lb)[4]) {
-  const uint32_t w0 = row_word<SM4, 4 * BLK + 0>(ra, off);
-  const uint32_t w1 = row_word<SM4, 4 * BLK + 1>(ra, off);
-  const uint32_t w2 = row_word<SM4, 4 * BLK + 2>(ra, off);
-  const uint32_t w3 = row_word<SM4, 4 * BLK + 3>(ra, off);
+template <int SM4, int BLK, bool LPART, uint32_t OFF>
+__device__ __forceinline__ void encode_block(const RowAddr<SM4>& ra, const bool (&pm)[4],
+                                             uint32_t& bad, uint32_t (&hb)[4],
+                                             uint32_t (&lb)[4]) {
+  const uint32_t w0 = row_word<SM4, 4 * BLK + 0, OFF>(ra);
+  const uint32_t w1 = row_word<SM4, 4 * BLK + 1, OFF>(ra);
+  const uint32_t w2 = row_word<SM4, 4 * BLK + 2, OFF>(ra);
+  const uint32_t w3 = row_word<SM4, 4 * BLK + 3, OFF>(ra);
   const uint32_t t0 = __byte_perm(w0, w1, 0x5140);
   const uint32_t t1 = __byte_perm(w0, w1, 0x7362);
   const uint32_t t2 = __byte_perm(w2, w3, 0x5140);
@@ -187,11 +187,33 @@ __device__ __forceinline__ void encode_block(const RowAddr<SM4>& ra, uint32_t of
   }
 }
 
-// Encode all quads of the lane for the staged group at buffer offset `boff`.
+template <int SM4, bool LPART, uint32_t OFF, typename Emit>
+__device__ __forceinline__ void encode_quad(const RowAddr<SM4>& ra, int q, int rem,
+                                            uint32_t (&bad)[8], Emit&& emit) {
+  bool pm[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) pm[m] = m < rem;
+  uint32_t hb[4] = {0u, 0u, 0u, 0u}, lb[4] = {0u, 0u, 0u, 0u};
+  encode_block<SM4, 7, LPART, OFF>(ra, pm, bad[7], hb, lb);
+  encode_block<SM4, 6, LPART, OFF>(ra, pm, bad[6], hb, lb);
+  encode_block<SM4, 5, LPART, OFF>(ra, pm, bad[5], hb, lb);
+  encode_block<SM4, 4, LPART, OFF>(ra, pm, bad[4], hb, lb);
+  encode_block<SM4, 3, LPART, OFF>(ra, pm, bad[3], hb, lb);
+  encode_block<SM4, 2, LPART, OFF>(ra, pm, bad[2], hb, lb);
+  encode_block<SM4, 1, LPART, OFF>(ra, pm, bad[1], hb, lb);
+  encode_block<SM4, 0, LPART, OFF>(ra, pm, bad[0], hb, lb);
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+    if (m < rem) emit(q, m, hb[m], hb[m] ^ lb[m]);  // paper code: high = b2, low = b1^b2
+}
+
+// Encode all quads of the lane for the staged group at buffer offset BOFF
+// (compile-time, like the quad offsets: the 32 row addresses stay in registers
+// and every LDS uses an immediate offset).
 // emit(q, m, hi_plane, lo_plane) for every position 4q+m < len.
-template <int SM4, bool LPART, int NIT, typename Emit>
-__device__ __forceinline__ uint32_t encode_group_v2(const RowAddr<SM4>& ra, uint32_t boff,
-                                                    int len, Emit&& emit) {
+template <int SM4, bool LPART, int NIT, uint32_t BOFF, typename Emit>
+__device__ __forceinline__ uint32_t encode_group_v2(const RowAddr<SM4>& ra, int len,
+                                                    Emit&& emit) {
   const int lane = threadIdx.x & 31;
   const int nquads = (len + 3) >> 2;
   uint32_t bad[8];
@@ -202,22 +224,10 @@ __device__ __forceinline__ uint32_t encode_group_v2(const RowAddr<SM4>& ra, uint
     const int q = lane + 32 * it;
     if (q < nquads) {
       const int rem = len - 4 * q;
-      bool pm[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) pm[m] = m < rem;
-      uint32_t hb[4] = {0u, 0u, 0u, 0u}, lb[4] = {0u, 0u, 0u, 0u};
-      const uint32_t off = boff + 128u * it;
-      encode_block<SM4, 7, LPART>(ra, off, pm, bad[7], hb, lb);
-      encode_block<SM4, 6, LPART>(ra, off, pm, bad[6], hb, lb);
-      encode_block<SM4, 5, LPART>(ra, off, pm, bad[5], hb, lb);
-      encode_block<SM4, 4, LPART>(ra, off, pm, bad[4], hb, lb);
-      encode_block<SM4, 3, LPART>(ra, off, pm, bad[3], hb, lb);
-      encode_block<SM4, 2, LPART>(ra, off, pm, bad[2], hb, lb);
-      encode_block<SM4, 1, LPART>(ra, off, pm, bad[1], hb, lb);
-      encode_block<SM4, 0, LPART>(ra, off, pm, bad[0], hb, lb);
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-        if (m < rem) emit(q, m, hb[m], hb[m] ^ lb[m]);  // paper code: high = b2, low = b1^b2
+      if (it == 0) encode_quad<SM4, LPART, BOFF>(ra, q, rem, bad, emit);
+      else if (it == 1) encode_quad<SM4, LPART, BOFF + 128u>(ra, q, rem, bad, emit);
+      else if (it == 2) encode_quad<SM4, LPART, BOFF + 256u>(ra, q, rem, bad, emit);
+      else encode_quad<SM4, LPART, BOFF + 384u>(ra, q, rem, bad, emit);
     }
   }
   uint32_t und = 0u;

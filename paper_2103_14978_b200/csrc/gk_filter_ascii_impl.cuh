@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(128) filter_ascii_kernel(
 // that the next span lands while the current one is encoded.  The encoder is
 // the one of gk_encode (encode_group_v2), emitting into the shared packed tile.
 // Phase 2 as in the generic kernel.
-template <int SM4, bool LPART, int NIT>
+template <int SM4, bool LPART, int NIT, uint32_t BUFB>
 __device__ __forceinline__ void ascii_phase1(const uint8_t* __restrict__ reads,
                                              const uint8_t* __restrict__ refs, int stride,
                                              int len, int64_t gbase, uint2* pq, uint2* pr,
@@ -198,9 +198,9 @@ __device__ __forceinline__ void ascii_phase1(const uint8_t* __restrict__ reads,
     mbar_wait(&bars[b], (uint32_t)(k >> 1) & 1u);
     const int gl = warp + 4 * (k >> 1);
     uint2* dst = (b ? pr : pq) + gl;
-    const uint32_t uu = encode_group_v2<SM4, LPART, NIT>(
-        ra, b * buf_bytes, len,
-        [&](int q, int m, uint32_t hi, uint32_t lo) { dst[(4 * q + m) * P] = make_uint2(hi, lo); });
+    auto emit = [&](int q, int m, uint32_t hi, uint32_t lo) { dst[(4 * q + m) * P] = make_uint2(hi, lo); };
+    const uint32_t uu = b == 0 ? encode_group_v2<SM4, LPART, NIT, 0u>(ra, len, emit)
+                               : encode_group_v2<SM4, LPART, NIT, BUFB>(ra, len, emit);
     u |= uu;
     if (b) {
       if (lane == 0) und[gl] = u;
@@ -238,14 +238,14 @@ __global__ void __launch_bounds__(128) filter_ascii_tma_kernel(
   uint8_t* mystg = stg + (size_t)warp * 2 * BUF;
   const bool lpart = (len & 3) != 0;
   switch ((stride & 3) * 2 + (lpart ? 1 : 0)) {
-    case 0: ascii_phase1<0, false, NIT>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 1: ascii_phase1<0, true, NIT>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 2: ascii_phase1<1, false, NIT>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 3: ascii_phase1<1, true, NIT>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 4: ascii_phase1<2, false, NIT>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 5: ascii_phase1<2, true, NIT>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 6: ascii_phase1<3, false, NIT>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    default: ascii_phase1<3, true, NIT>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
+    case 0: ascii_phase1<0, false, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
+    case 1: ascii_phase1<0, true, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
+    case 2: ascii_phase1<1, false, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
+    case 3: ascii_phase1<1, true, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
+    case 4: ascii_phase1<2, false, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
+    case 5: ascii_phase1<2, true, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
+    case 6: ascii_phase1<3, false, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
+    default: ascii_phase1<3, true, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
   }
   __syncthreads();
 
