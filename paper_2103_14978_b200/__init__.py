@@ -56,6 +56,8 @@ def load_library(path: str = LIB_PATH):
         "gk_compact": (ctypes.c_int, [P, I64, P, P, P, SZ, P]),
         "gk_host_workspace_bytes": (SZ, [I64, I64]),
         "gk_filter_host": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P, SZ, I64]),
+        "gk_host_sweep_workspace_bytes": (SZ, [I64, I64, I32, I32]),
+        "gk_filter_host_sweep": (ctypes.c_int, [P, P, I64, I64, I32, P, I32, P, P, P, SZ, I64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -190,4 +192,31 @@ def filter_host(reads, refs, e: int, length: int | None = None, accept=None, err
                                          accept.data_ptr(), _ptr(errcount),
                                          workspace.data_ptr(), workspace.numel(), chunk_pairs),
            "gk_filter_host")
+    return accept, errcount
+
+
+def host_sweep_workspace_bytes(chunk_pairs: int, stride: int, length: int, n_e: int) -> int:
+    return load_library().gk_host_sweep_workspace_bytes(chunk_pairs, stride, length, n_e)
+
+
+def filter_host_sweep(reads, refs, e_list, length: int | None = None, accept=None,
+                      errcount=None, workspace=None, chunk_pairs: int = 1 << 20):
+    """Threshold sweep of HOST uint8 tensors: each chunk is copied and encoded once, then
+    filtered for every e.  Returns (accept bits [n_e, words], errcount [n_e, n] or None)."""
+    import torch
+    n, stride = reads.shape
+    length = stride if length is None else length
+    es = (ctypes.c_int32 * len(e_list))(*e_list)
+    if accept is None:
+        accept = torch.empty((len(e_list), max(1, result_words(n))), dtype=torch.int32,
+                             pin_memory=True)
+    if workspace is None:
+        workspace = torch.empty(host_sweep_workspace_bytes(chunk_pairs, stride, length,
+                                                           len(e_list)),
+                                dtype=torch.uint8, device="cuda")
+    _check(load_library().gk_filter_host_sweep(reads.data_ptr(), refs.data_ptr(), stride, n,
+                                               length, es, len(e_list), accept.data_ptr(),
+                                               _ptr(errcount), workspace.data_ptr(),
+                                               workspace.numel(), chunk_pairs),
+           "gk_filter_host_sweep")
     return accept, errcount

@@ -205,4 +205,95 @@ int gk_filter_host(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride
   return rc;
 }
 
+// ---- host-buffer threshold sweep ---------------------------------------------
+struct SweepLayout {
+  size_t in, packed, undef, acc, err, per_set;
+};
+
+static SweepLayout sweep_layout(int64_t chunk, int64_t stride, int32_t len, int32_t n_e) {
+  SweepLayout L;
+  L.in = round_up((size_t)chunk * (size_t)stride, 256);
+  L.packed = round_up(gk_packed_words(chunk, len) * 4, 256);
+  L.undef = round_up(gk_undef_words(chunk) * 4, 256);
+  L.acc = round_up((size_t)(chunk / 32 + 1) * 4, 256);
+  L.err = round_up((size_t)chunk, 256);
+  L.per_set = 2 * L.in + 2 * L.packed + 2 * L.undef + (size_t)n_e * (L.acc + L.err);
+  return L;
+}
+
+size_t gk_host_sweep_workspace_bytes(int64_t chunk_pairs, int64_t stride, int32_t len,
+                                     int32_t n_e) {
+  if (chunk_pairs <= 0 || stride <= 0 || len <= 0 || n_e <= 0) return 0;
+  return 2 * sweep_layout(chunk_pairs, stride, len, n_e).per_set;
+}
+
+int gk_filter_host_sweep(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride,
+                         int64_t n_pairs, int32_t len, const int32_t* e_list, int32_t n_e,
+                         uint32_t* h_accept_bits, uint8_t* h_errcount, void* d_ws,
+                         size_t ws_bytes, int64_t chunk_pairs) {
+  int rc = check_ascii(h_reads, n_pairs, len, stride);
+  if (rc) return rc;
+  if (n_e <= 0 || !e_list) return GK_ERR_ARG;
+  for (int t = 0; t < n_e; ++t)
+    if (e_list[t] < 0 || e_list[t] >= len) return GK_ERR_E;
+  if (n_pairs == 0) return GK_OK;
+  if (!h_refs || !h_accept_bits) return GK_ERR_ARG;
+  if (chunk_pairs <= 0 || chunk_pairs % 1024 != 0) return GK_ERR_ARG;
+  if (!d_ws || ws_bytes < gk_host_sweep_workspace_bytes(chunk_pairs, stride, len, n_e))
+    return GK_ERR_WORKSPACE;
+  if (!aligned(d_ws, 256)) return GK_ERR_ALIGN;
+  const SweepLayout L = sweep_layout(chunk_pairs, stride, len, n_e);
+  const size_t words_total = gk_result_words(n_pairs);
+  cudaStream_t st[2];
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t err = cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking);
+    if (err != cudaSuccess) {
+      if (b == 1) cudaStreamDestroy(st[0]);
+      return cuda_status(err);
+    }
+  }
+  rc = GK_OK;
+  const int64_t nchunks = (n_pairs + chunk_pairs - 1) / chunk_pairs;
+  for (int64_t c = 0; c < nchunks && rc == GK_OK; ++c) {
+    const int b = (int)(c & 1);
+    uint8_t* base = static_cast<uint8_t*>(d_ws) + b * L.per_set;
+    uint8_t* dr = base;
+    uint8_t* df = dr + L.in;
+    uint32_t* pq = reinterpret_cast<uint32_t*>(df + L.in);
+    uint32_t* pr = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(pq) + L.packed);
+    uint32_t* uq = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(pr) + L.packed);
+    uint32_t* ur = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(uq) + L.undef);
+    uint8_t* outs = reinterpret_cast<uint8_t*>(ur) + L.undef;
+    const int64_t p0 = c * chunk_pairs;
+    const int64_t np = (n_pairs - p0) < chunk_pairs ? (n_pairs - p0) : chunk_pairs;
+    const size_t bytes = (size_t)((np - 1) * stride + len);
+    cudaError_t err = cudaMemcpyAsync(dr, h_reads + p0 * stride, bytes, cudaMemcpyHostToDevice,
+                                      st[b]);
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(df, h_refs + p0 * stride, bytes, cudaMemcpyHostToDevice, st[b]);
+    if (err != cudaSuccess) { rc = cuda_status(err); break; }
+    gk::launch_encode(dr, np, len, stride, pq, uq, st[b]);
+    gk::launch_encode(df, np, len, stride, pr, ur, st[b]);
+    for (int t = 0; t < n_e && rc == GK_OK; ++t) {
+      uint32_t* acc = reinterpret_cast<uint32_t*>(outs + (size_t)t * (L.acc + L.err));
+      uint8_t* ec = h_errcount ? reinterpret_cast<uint8_t*>(acc) + L.acc : nullptr;
+      gk::launch_filter(pq, pr, uq, ur, np, len, e_list[t], acc, ec, 0, st[b]);
+      rc = after_launch();
+      if (rc) break;
+      err = cudaMemcpyAsync(h_accept_bits + (size_t)t * words_total + p0 / 32, acc,
+                            (size_t)((np + 31) / 32) * 4, cudaMemcpyDeviceToHost, st[b]);
+      if (err == cudaSuccess && h_errcount)
+        err = cudaMemcpyAsync(h_errcount + (size_t)t * n_pairs + p0, ec, (size_t)np,
+                              cudaMemcpyDeviceToHost, st[b]);
+      if (err != cudaSuccess) rc = cuda_status(err);
+    }
+  }
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t err = cudaStreamSynchronize(st[b]);
+    if (rc == GK_OK && err != cudaSuccess) rc = cuda_status(err);
+    cudaStreamDestroy(st[b]);
+  }
+  return rc;
+}
+
 }  // extern "C"

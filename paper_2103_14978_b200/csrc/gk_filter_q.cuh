@@ -98,51 +98,82 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 }
 
 // Masks of one warp: optional Hamming mask, then D_k, I_k for k in [K0, K1].
+// The read words the masks need are kept in two register windows, as in
+// SinglePass<E>: the deletion window Q[p-K1 .. p-K0] and the insertion window
+// Q[p+K0 .. p+K1] (p = i + 2 is the newest position); each step shifts both by
+// one position and loads the new entries (Q[p-K0], Q[p+K1], and Q[p] for the
+// Hamming mask) from the shared TMA ring.
 template <bool WITH_H, int K0, int K1>
 struct MaskSetQ {
-  static constexpr int NK = K1 >= K0 ? K1 - K0 + 1 : 0;
+  static constexpr int NK = K1 - K0 + 1;
   static constexpr int NM = (WITH_H ? 1 : 0) + 2 * NK;
-  static constexpr int KMAX = NK > 0 ? K1 : 0;
-  uint32_t x[NM > 0 ? NM : 1][4];
+  static constexpr int KMAX = K1;
+  static constexpr int HB = WITH_H ? 1 : 0;
+  uint32_t x[NM][4];
+  uint32_t dh[NK], dl[NK];  // deletion window:  index j <-> Q[p - K1 + j]
+  uint32_t ih[NK], il[NK];  // insertion window: index j <-> Q[p + K0 + j]
 
   __device__ __forceinline__ static constexpr bool is_h(int m) { return WITH_H && m == 0; }
   __device__ __forceinline__ static constexpr int kk(int m) {
-    return is_h(m) ? 0 : K0 + ((m - (WITH_H ? 1 : 0)) >> 1);
+    return is_h(m) ? 0 : K0 + ((m - HB) >> 1);
   }
   __device__ __forceinline__ static constexpr bool is_d(int m) {
-    return !is_h(m) && (((m - (WITH_H ? 1 : 0)) & 1) == 0);
-  }
-  __device__ __forceinline__ static constexpr int qoff(int m) {
-    return is_h(m) ? 0 : (is_d(m) ? -kk(m) : kk(m));
+    return !is_h(m) && (((m - HB) & 1) == 0);
   }
 
   __device__ __forceinline__ void init() {
 #pragma unroll
     for (int m = 0; m < NM; ++m) x[m][0] = x[m][1] = x[m][2] = x[m][3] = 0u;
+#pragma unroll
+    for (int j = 0; j < NK; ++j) dh[j] = dl[j] = ih[j] = il[j] = 0u;
   }
 
-  // One step (p = i + 2).  F: AND of this warp's amended masks at i; A0: amended
-  // Hamming mask at i (WITH_H).  CHECKED: vacancy / range checks at run time.
+  __device__ __forceinline__ static uint2 qload(const QRing& ring, int pos, int len) {
+    return (pos >= 0 && pos < len) ? ring.q_at(pos) : make_uint2(0u, 0u);
+  }
+
+  // Fill the windows for a first step whose newest position is p0 (checked loads).
+  __device__ __forceinline__ void fill(const QRing& ring, int p0, int len) {
+#pragma unroll
+    for (int j = 0; j < NK; ++j) {
+      const uint2 d = qload(ring, p0 - 1 - K1 + j, len);
+      const uint2 v = qload(ring, p0 - 1 + K0 + j, len);
+      dh[j] = d.x; dl[j] = d.y;
+      ih[j] = v.x; il[j] = v.y;
+    }
+  }
+
+  // One step (p = i + 2): shift the windows in (qd = Q[p-K0], qi = Q[p+K1],
+  // q0 = Q[p]).  F: AND of this warp's amended masks at i; A0: amended Hamming
+  // mask at i.  CHECKED: vacancy / range checks at run time (head, tail).
   template <bool CHECKED, bool FIN>
-  __device__ __forceinline__ void step(const QRing& ring, int i, int len, uint2 rn,
-                                       const uint32_t* qb, int c, uint32_t& F, uint32_t& A0) {
+  __device__ __forceinline__ void step(int i, int len, uint2 rn, uint2 qd, uint2 qi, uint2 q0,
+                                       uint32_t& F, uint32_t& A0) {
     const int p = i + 2;
+#pragma unroll
+    for (int j = 0; j < NK - 1; ++j) {
+      dh[j] = dh[j + 1]; dl[j] = dl[j + 1];
+      ih[j] = ih[j + 1]; il[j] = il[j + 1];
+    }
+    dh[NK - 1] = qd.x; dl[NK - 1] = qd.y;
+    ih[NK - 1] = qi.x; il[NK - 1] = qi.y;
     F = 0xFFFFFFFFu;
     A0 = 0u;
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
-      uint32_t xn;
-      if constexpr (CHECKED) {
-        const int qp = p + qoff(m);
-        xn = 0u;
-        if (p >= 0 && p < len && qp >= 0 && qp < len) {
-          const uint2 q = ring.q_at(qp);
-          xn = mismatch(rn.x, rn.y, q.x, q.y);
-        }
+      uint32_t qh, ql;
+      if (is_h(m)) {
+        qh = q0.x; ql = q0.y;
+      } else if (is_d(m)) {
+        qh = dh[K1 - kk(m)]; ql = dl[K1 - kk(m)];
       } else {
-        const int cq = c + qoff(m);  // >= 0 by construction of qb
-        const uint2 q = QRing::lds(qb[cq >> 3] + (uint32_t)(cq & 7) * 256u);
-        xn = mismatch(rn.x, rn.y, q.x, q.y);
+        qh = ih[kk(m) - K0]; ql = il[kk(m) - K0];
+      }
+      uint32_t xn = mismatch(rn.x, rn.y, qh, ql);
+      if constexpr (CHECKED) {
+        const int qp = is_h(m) ? p : (is_d(m) ? p - kk(m) : p + kk(m));
+        const bool ok = p >= 0 && p < len && qp >= 0 && qp < len;
+        xn = ok ? xn : 0u;
       }
       if constexpr (FIN) {
         const uint32_t a = amend(x[m][0], x[m][1], x[m][2], x[m][3], xn);
@@ -158,43 +189,60 @@ struct MaskSetQ {
     }
   }
 
-  // 8 steps i = ib..ib+7 (ib % 8 == 0); checked decides the variant at run time.
+  template <bool CHECKED, bool FIN>
+  __device__ __forceinline__ void step_loading(const QRing& ring, int i, int len, uint32_t& F,
+                                               uint32_t& A0) {
+    const int p = i + 2;
+    const uint2 rn = (p >= 0 && p < len) ? ring.r_at(p) : make_uint2(0u, 0u);
+    const uint2 qd = qload(ring, p - K0, len);
+    const uint2 qi = qload(ring, p + K1, len);
+    const uint2 q0 = WITH_H ? qload(ring, p, len) : make_uint2(0u, 0u);
+    step<CHECKED, FIN>(i, len, rn, qd, qi, q0, F, A0);
+  }
+
+  // 8 steps i = ib..ib+7 (ib % 8 == 0); `checked` selects the variant at run time.
   __device__ __forceinline__ void block(const QRing& ring, int ib, int len, bool checked,
                                         uint32_t (&F)[8], uint32_t (&A0)[8]) {
-    constexpr int LO = (2 - KMAX) >> 3;  // floor((2-KMAX)/8)
-    constexpr int HI = (9 + KMAX) >> 3;
-    constexpr int NB = HI - LO + 1;
     if (!checked) {
+      // all positions valid: ring addresses from per-block slot bases + immediates
       const int bi = ib >> 3;
+      constexpr int CD0 = 2 - K0;       // c of Q[p - K0] at u = 0 (p = ib + 2 + u)
+      constexpr int CI0 = 2 + K1;       // c of Q[p + K1]
+      constexpr int LO = (CD0 < 2 ? CD0 : 2) >> 3;
+      constexpr int HI = (CI0 + 7) >> 3;
+      constexpr int NB = HI - LO + 1;
       uint32_t qb[NB];
 #pragma unroll
       for (int d = 0; d < NB; ++d)
         qb[d] = ring.qsm + (uint32_t)((bi + LO + d) & (QR_SLOTS - 1)) * 2048u;
       const uint32_t rb0 = ring.rsm + (uint32_t)(bi & (RR_SLOTS - 1)) * 2048u;
       const uint32_t rb1 = ring.rsm + (uint32_t)((bi + 1) & (RR_SLOTS - 1)) * 2048u;
+      auto qat = [&](int c) -> uint2 {  // Q[ib + c], c static
+        const int cc = c - 8 * LO;
+        return QRing::lds(qb[cc >> 3] + (uint32_t)(cc & 7) * 256u);
+      };
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int c = u + 2;
         const uint2 rn = c < 8 ? QRing::lds(rb0 + c * 256u) : QRing::lds(rb1 + (c - 8) * 256u);
-        step<false, true>(ring, ib + u, len, rn, qb, c - 8 * LO, F[u], A0[u]);
+        const uint2 qd = qat(c - K0);
+        const uint2 qi = qat(c + K1);
+        const uint2 q0 = WITH_H ? qat(c) : make_uint2(0u, 0u);
+        step<false, true>(ib + u, len, rn, qd, qi, q0, F[u], A0[u]);
       }
     } else {
 #pragma unroll 1
-      for (int u = 0; u < 8; ++u) {
-        const int p = ib + u + 2;
-        const uint2 rn = (p < len) ? ring.r_at(p) : make_uint2(0u, 0u);
-        step<true, true>(ring, ib + u, len, rn, nullptr, 0, F[u], A0[u]);
-      }
+      for (int u = 0; u < 8; ++u) step_loading<true, true>(ring, ib + u, len, F[u], A0[u]);
     }
   }
 
-  // priming: make x at p = -2..1 the window contents (no finalize)
+  // priming: windows for p0 = -2, then x at p = -2..1 (no finalize)
   __device__ __forceinline__ void prime(const QRing& ring, int len) {
+    fill(ring, -2, len);
+#pragma unroll 1
     for (int i = -4; i < 0; ++i) {
-      const int p = i + 2;
-      const uint2 rn = (p >= 0 && p < len) ? ring.r_at(p) : make_uint2(0u, 0u);
       uint32_t F, A0;
-      step<true, false>(ring, i, len, rn, nullptr, 0, F, A0);
+      step_loading<true, false>(ring, i, len, F, A0);
     }
   }
 };

@@ -74,6 +74,12 @@ def test_argument_validation_before_any_launch(lib):
     assert lib.gk_compact(P, 1 << 33, P, P, P, 1 << 20, None) == -1
     assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 1 << 30, 1000) == -1  # chunk
     assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 10, 1024) == -5
+    import ctypes as C
+    es = (C.c_int32 * 2)(1, 100)
+    assert lib.gk_filter_host_sweep(P, P, 100, 10, 100, es, 2, P, None, P, 1 << 30, 1024) == -3
+    es = (C.c_int32 * 2)(1, 5)
+    assert lib.gk_filter_host_sweep(P, P, 100, 10, 100, es, 2, P, None, P, 10, 1024) == -5
+    assert lib.gk_filter_host_sweep(P, P, 100, 10, 100, es, 0, P, None, P, 10, 1024) == -1
 
 
 def test_product_package_does_not_import_the_oracle():

@@ -208,6 +208,19 @@ def test_filter_host_end_to_end(gk):
     assert (err.numpy() == oc).all()
 
 
+def test_filter_host_sweep(gk):
+    n, L, es = 70_000, 150, [0, 3, 7, 12, 15]
+    reads, refs = pairgen.gen_pairs(n, L)
+    hr = torch.from_numpy(reads).pin_memory()
+    hf = torch.from_numpy(refs).pin_memory()
+    err = torch.empty((len(es), n), dtype=torch.uint8).pin_memory()
+    acc, _ = gk.filter_host_sweep(hr, hf, es, errcount=err, chunk_pairs=16384)
+    oa, oc = oracle.sweep(reads, refs, max(es))
+    for t, e in enumerate(es):
+        assert (unpack_accept(acc[t], n) == oa[e]).all(), e
+        assert (err[t].numpy() == oc[e]).all(), e
+
+
 # ---------------------------------------------------------------- full size ----
 @pytest.mark.parametrize("L,e", [(100, 5), (150, 7), (250, 12)])
 def test_full_size_sampled(gk, L, e):
