@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(128) filter_sp_kernel(
 __global__ void __launch_bounds__(128) filter_generic_kernel(
     const uint2* __restrict__ reads, const uint2* __restrict__ refs,
     const uint32_t* __restrict__ rund, const uint32_t* __restrict__ fund, int64_t n, int len,
-    int e, uint32_t* __restrict__ accept, uint8_t* __restrict__ errc) {
+    int e, uint32_t* __restrict__ accept, uint8_t* __restrict__ errc, int edge_fix) {
   extern __shared__ uint32_t sm_f[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(128) filter_generic_kernel(
   src.len = len;
   const uint32_t undef = __ldg(rund + g) | __ldg(fund + g);
   uint32_t cA[8], cF[8];
-  generic_group(src, len, e, undef, sm_f + (size_t)warp * len * 32 + lane, 32, cA, cF);
+  generic_group(src, len, e, undef, sm_f + (size_t)warp * len * 32 + lane, 32, cA, cF,
+                edge_fix != 0);
   finish_group(cA, cF, e, undef, g, n, accept, errc);
 }
 
@@ -138,7 +139,9 @@ static bool dispatch_spq(int e, const uint2* reads, const uint2* refs, const uin
 
 int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* rund,
                   const uint32_t* fund, int64_t n, int len, int e, uint32_t* accept,
-                  uint8_t* errc, int force_generic, cudaStream_t stream) {
+                  uint8_t* errc, int flags, cudaStream_t stream) {
+  const int force_generic = flags & 3;  // GK_FLAG_GENERIC | GK_FLAG_NO_EDGE_FIX
+  const int edge_fix = (flags & 2) ? 0 : 1;
   const uint2* r2 = reinterpret_cast<const uint2*>(reads);
   const uint2* f2 = reinterpret_cast<const uint2*>(refs);
   if (!force_generic &&
@@ -157,7 +160,8 @@ int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* r
                          (int)smem);
   const int64_t blocks = (tiles + warps - 1) / warps;
   filter_generic_kernel<<<(unsigned)blocks, warps * 32, smem, stream>>>(r2, f2, rund, fund, n,
-                                                                        len, e, accept, errc);
+                                                                        len, e, accept, errc,
+                                                                        edge_fix);
   return 0;
 }
 

@@ -364,7 +364,7 @@ __device__ __forceinline__ void finish_group(const uint32_t (&cA)[8], const uint
 template <class Src>
 __device__ __forceinline__ void generic_group(const Src& src, int len, int e, uint32_t undef,
                                               uint32_t* F, int fstride, uint32_t (&c0)[8],
-                                              uint32_t (&cf)[8]) {
+                                              uint32_t (&cf)[8], bool edge_fix = true) {
   auto xmask = [&](int p, int shift, int lo, int hi) -> uint32_t {
     if (p < lo || p >= hi) return 0u;
     const uint2 q = src.ldq(p - shift);
@@ -391,8 +391,10 @@ __device__ __forceinline__ void generic_group(const Src& src, int len, int e, ui
   if (e > 0 && (early | undef) != 0xFFFFFFFFu) {
     for (int k = 1; k <= e; ++k) {
       {  // deletion mask D_k: valid positions [k, len); positions < k forced to 1
-        uint32_t xm2 = 0u, xm1 = 0u, x0 = xmask(k, k, k, len), xp1 = xmask(k + 1, k, k, len);
-        for (int i = k; i < len; ++i) {
+         // (edge fix) -- or, original GateKeeper, left at their amended 0
+        const int i0 = edge_fix ? k : 0;
+        uint32_t xm2 = 0u, xm1 = 0u, x0 = xmask(i0, k, k, len), xp1 = xmask(i0 + 1, k, k, len);
+        for (int i = i0; i < len; ++i) {
           const uint32_t xp2 = xmask(i + 2, k, k, len);
           F[i * fstride] &= amend(xm2, xm1, x0, xp1, xp2);
           xm2 = xm1; xm1 = x0; x0 = xp1; xp1 = xp2;
@@ -400,8 +402,9 @@ __device__ __forceinline__ void generic_group(const Src& src, int len, int e, ui
       }
       {  // insertion mask I_k: valid positions [0, len-k); positions >= len-k forced to 1
         const int hi = len - k;
+        const int i1 = edge_fix ? hi : len;
         uint32_t xm2 = 0u, xm1 = 0u, x0 = xmask(0, -k, 0, hi), xp1 = xmask(1, -k, 0, hi);
-        for (int i = 0; i < hi; ++i) {
+        for (int i = 0; i < i1; ++i) {
           const uint32_t xp2 = xmask(i + 2, -k, 0, hi);
           F[i * fstride] &= amend(xm2, xm1, x0, xp1, xp2);
           xm2 = xm1; xm1 = x0; x0 = xp1; xp1 = xp2;

@@ -17,7 +17,7 @@ int launch_encode(const uint8_t* seqs, int64_t n, int len, int64_t stride, uint3
 
 int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* rund,
                   const uint32_t* fund, int64_t n, int len, int e, uint32_t* accept,
-                  uint8_t* errc, int force_generic, cudaStream_t stream);
+                  uint8_t* errc, int flags, cudaStream_t stream);
 
 int launch_filter_ascii(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n,
                         int len, int e, uint32_t* accept, uint8_t* errc, cudaStream_t stream);

@@ -181,3 +181,21 @@ def test_lowercase_is_same_base():
         a0, c0 = oracle.filter(q, r, e)
         a1, c1 = oracle.filter(q | 0x20, r, e)
         assert (a0 == a1).all() and (c0 == c1).all()
+
+
+def test_edge_fix_reduces_false_accepts():
+    """P11: GateKeeper-GPU's edge fix rejects pairs GateKeeper falsely accepts
+     -- never the reverse on an accept that is correct, and
+    in aggregate fewer false accepts."""
+    reads, refs = pairgen.gen_pairs(6000, 100, seed=3)
+    dist = oracle.edit_distance(reads, refs)
+    for e in (2, 5, 8):
+        a_gpu, c_gpu = oracle.filter(reads, refs, e, edge_fix=True)
+        a_gk, _ = oracle.filter(reads, refs, e, edge_fix=False)
+        defined = c_gpu != 255
+        fa_gpu = ((a_gpu == 1) & (dist > e) & defined).sum()
+        fa_gk = ((a_gk == 1) & (dist > e) & defined).sum()
+        assert fa_gpu <= fa_gk
+        # forcing the vacated bits to 1 can only add 1s to the AND (more errors); it
+        # must still never reject a pair within edit distance e (:224, :530)
+        assert ((a_gpu == 0) & (dist <= e) & defined).sum() == 0

@@ -155,6 +155,20 @@ def test_ragged_counts(gk):
             assert_parity(gk, reads, refs, e, path="ascii")
 
 
+@pytest.mark.parametrize("L", [17, 100, 150])
+def test_original_gatekeeper_flag(gk, L):
+    """GK_FLAG_NO_EDGE_FIX = original GateKeeper (oracle edge_fix=False)."""
+    reads, refs = pairgen.gen_pairs(3000, L, profile=pairgen.PROFILE_BALANCED, emax=L // 10 + 1,
+                                    seed=L + 99)
+    for e in (0, 1, 2, L // 10, L // 5):
+        if e >= L:
+            continue
+        a, c = run_filter(gk, reads, refs, e, flags=gk.GK_FLAG_NO_EDGE_FIX)
+        oa, oc = oracle.filter(reads, refs, e, edge_fix=False)
+        bad = np.nonzero((a != oa) | (c != oc))[0]
+        assert bad.size == 0, (L, e, bad[:5])
+
+
 def test_no_errcount_output(gk):
     reads, refs = pairgen.gen_pairs(3000, 100)
     dr, df = to_dev(reads), to_dev(refs)
@@ -246,3 +260,17 @@ def test_full_size_sampled(gk, L, e):
         bits = np.unpackbits(acc_all[s // 32:(s + 4096) // 32].view(np.uint8), bitorder="little")
         assert (bits == oa).all() and (err_all[s:s + 4096] == oc).all(), s
     del dr, df, q, r
+
+
+# ---------------------------------------------------------------- sanitizers ---
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer(gk, tool):
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = ["compute-sanitizer", "--tool", tool, "--error-exitcode", "3", "python",
+           os.path.join(root, "tools", "sanitize_run.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=root)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0 and "sanitize_run ok" in out, out[-3000:]
+    assert ("ERROR SUMMARY: 0 errors" in out or "(0 errors, 0 warnings)" in out), out[-3000:]
