@@ -94,7 +94,9 @@ struct QRing {
 };
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  __syncwarp();
+  // non-.aligned form: the two warps of a pair reach it from different code
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // Masks of one warp: optional Hamming mask, then D_k, I_k for k in [K0, K1].

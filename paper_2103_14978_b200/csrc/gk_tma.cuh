@@ -38,6 +38,10 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
+// Wait for the phase with parity `phase` of `bar` to complete.  Called by whole
+// warps; the lanes leave the try_wait loop independently, so the warp is
+// reconverged before returning (later warp-collective / barrier instructions are
+// .aligned).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n"
@@ -48,6 +52,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+  __syncwarp();
 }
 
 }  // namespace gk
