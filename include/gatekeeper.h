@@ -114,9 +114,13 @@ int gk_filter(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
  * ORIGINAL GateKeeper (Alser et al. 2017; PAPER.md Fig. S.1): the vacated
  * leading / trailing bits of the shifted masks stay at their amended value 0
  * instead of being ORed to 1 -- for A/B accuracy studies
- * (:136, :238); it runs on the mask-major kernel. */
+ * (:136, :238); it runs on the block-transposed kernel. */
 #define GK_FLAG_GENERIC 1
 #define GK_FLAG_NO_EDGE_FIX 2
+/* GK_FLAG_BLOCKED forces the block-transposed kernel (8-position blocks x all
+ * masks, any e; the default for e above the all-register instantiations) --
+ * diagnostic / test knob: results are identical. */
+#define GK_FLAG_BLOCKED 4
 int gk_filter_ex(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
                  const uint32_t* d_read_undef, const uint32_t* d_ref_undef,
                  int64_t n_pairs, int32_t len, int32_t e,

@@ -23,6 +23,7 @@ GK_MAX_STRIDE = 1024
 GK_TILE = 1024
 GK_FLAG_GENERIC = 1
 GK_FLAG_NO_EDGE_FIX = 2
+GK_FLAG_BLOCKED = 4
 
 _lib = None
 

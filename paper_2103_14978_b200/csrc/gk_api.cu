@@ -87,7 +87,7 @@ int gk_filter_ex(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
       !aligned(d_ref_undef, 4) || !aligned(d_accept_bits, 4))
     return GK_ERR_ALIGN;
   gk::launch_filter(d_reads_packed, d_refs_packed, d_read_undef, d_ref_undef, n_pairs, len, e,
-                    d_accept_bits, d_errcount, flags & (GK_FLAG_GENERIC | GK_FLAG_NO_EDGE_FIX),
+                    d_accept_bits, d_errcount, flags & (GK_FLAG_GENERIC | GK_FLAG_NO_EDGE_FIX | GK_FLAG_BLOCKED),
                     (cudaStream_t)stream);
   return after_launch();
 }

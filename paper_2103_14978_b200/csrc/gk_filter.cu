@@ -137,13 +137,21 @@ static bool dispatch_spq(int e, const uint2* reads, const uint2* refs, const uin
   return false;
 }
 
+void launch_bt(const uint2* reads, const uint2* refs, const uint32_t* rund, const uint32_t* fund,
+               int64_t n, int len, int e, uint32_t* accept, uint8_t* errc, int edge_fix,
+               cudaStream_t stream);
+
 int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* rund,
                   const uint32_t* fund, int64_t n, int len, int e, uint32_t* accept,
                   uint8_t* errc, int flags, cudaStream_t stream) {
-  const int force_generic = flags & 3;  // GK_FLAG_GENERIC | GK_FLAG_NO_EDGE_FIX
-  const int edge_fix = (flags & 2) ? 0 : 1;
+  const int force_generic = flags & 1;  // GK_FLAG_GENERIC
+  const int edge_fix = (flags & 2) ? 0 : 1;  // GK_FLAG_NO_EDGE_FIX
   const uint2* r2 = reinterpret_cast<const uint2*>(reads);
   const uint2* f2 = reinterpret_cast<const uint2*>(refs);
+  if (!force_generic && ((flags & 4) || !edge_fix)) {  // GK_FLAG_BLOCKED, or original GateKeeper
+    launch_bt(r2, f2, rund, fund, n, len, e, accept, errc, edge_fix, stream);
+    return 0;
+  }
   if (!force_generic &&
       dispatch_sp<GK_SP_EMAX>(e, r2, f2, rund, fund, n, len, accept, errc, stream))
     return 0;

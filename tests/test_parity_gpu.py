@@ -106,8 +106,8 @@ def test_paper_profile_e_sweep(gk, L):
     emax = {100: 10, 150: 15, 250: 25}[L]
     oa, oc = oracle.sweep(reads, refs, emax)
     for e in range(emax + 1):
-        for path, flags in (("packed", 0), ("ascii", 0), ("packed", 1)):
-            if flags and e % 3:
+        for path, flags in (("packed", 0), ("ascii", 0), ("packed", 1), ("packed", 4)):
+            if flags == 1 and e % 3:
                 continue
             a, c = run_filter(gk, reads, refs, e, flags=flags, path=path)
             bad = np.nonzero((a != oa[e]) | (c != oc[e]))[0]
@@ -123,6 +123,7 @@ def test_random_lengths(gk, L):
     for e in es:
         assert_parity(gk, reads, refs, e, path="packed")
         assert_parity(gk, reads, refs, e, path="ascii")
+        assert_parity(gk, reads, refs, e, path="packed", flags=gk.GK_FLAG_BLOCKED)
 
 
 def test_adversarial_sets(gk):
@@ -144,6 +145,7 @@ def test_adversarial_sets(gk):
         for e in (0, 1, 2, 4, 8, 15, 23, 47):
             assert_parity(gk, reads, refs, e, path="packed")
             assert_parity(gk, reads, refs, e, path="ascii")
+            assert_parity(gk, reads, refs, e, path="packed", flags=gk.GK_FLAG_BLOCKED)
 
 
 def test_ragged_counts(gk):
@@ -153,6 +155,7 @@ def test_ragged_counts(gk):
         for e in (0, 3, 14):
             assert_parity(gk, reads, refs, e, path="packed")
             assert_parity(gk, reads, refs, e, path="ascii")
+            assert_parity(gk, reads, refs, e, path="packed", flags=gk.GK_FLAG_BLOCKED)
 
 
 @pytest.mark.parametrize("L", [17, 100, 150])
