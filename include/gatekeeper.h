@@ -109,8 +109,8 @@ int gk_filter(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
               uint32_t* d_accept_bits, uint8_t* d_errcount, void* stream);
 
 /* gk_filter with option flags.  GK_FLAG_GENERIC forces the mask-major fallback
- * kernel that otherwise only serves e above the register-resident instantiations
- * (diagnostic / test knob: results are identical).  GK_FLAG_NO_EDGE_FIX runs the
+ * kernel (F kept in shared memory, one mask at a time; never the default --
+ * diagnostic / test knob: results are identical).  GK_FLAG_NO_EDGE_FIX runs the
  * ORIGINAL GateKeeper (Alser et al. 2017; PAPER.md Fig. S.1): the vacated
  * leading / trailing bits of the shifted masks stay at their amended value 0
  * instead of being ORed to 1 -- for A/B accuracy studies

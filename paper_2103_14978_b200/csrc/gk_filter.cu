@@ -120,23 +120,6 @@ static bool dispatch_sp(int e, const uint2* reads, const uint2* refs, const uint
   return false;
 }
 
-template <int E>
-void launch_spq(const uint2* reads, const uint2* refs, const uint32_t* rund, const uint32_t* fund,
-                int64_t n, int len, uint32_t* accept, uint8_t* errc, cudaStream_t stream);
-
-template <int E>
-static bool dispatch_spq(int e, const uint2* reads, const uint2* refs, const uint32_t* rund,
-                         const uint32_t* fund, int64_t n, int len, uint32_t* accept,
-                         uint8_t* errc, cudaStream_t stream) {
-  if (e == E) {
-    launch_spq<E>(reads, refs, rund, fund, n, len, accept, errc, stream);
-    return true;
-  }
-  if constexpr (E > GK_SP_EMAX + 1)
-    return dispatch_spq<E - 1>(e, reads, refs, rund, fund, n, len, accept, errc, stream);
-  return false;
-}
-
 void launch_bt(const uint2* reads, const uint2* refs, const uint32_t* rund, const uint32_t* fund,
                int64_t n, int len, int e, uint32_t* accept, uint8_t* errc, int edge_fix,
                cudaStream_t stream);
@@ -148,15 +131,16 @@ int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* r
   const int edge_fix = (flags & 2) ? 0 : 1;  // GK_FLAG_NO_EDGE_FIX
   const uint2* r2 = reinterpret_cast<const uint2*>(reads);
   const uint2* f2 = reinterpret_cast<const uint2*>(refs);
-  if (!force_generic && ((flags & 4) || !edge_fix)) {  // GK_FLAG_BLOCKED, or original GateKeeper
+  // e <= GK_SP_EMAX: the all-register single pass; above it (and for the
+  // original GateKeeper, or on request) the block-transposed kernel, which
+  // measured 1.3-1.7x faster than the earlier warp-pair split at e = 12..25
+  // (profiles/r01_cmp_bt.jsonl)
+  if (!force_generic && ((flags & 4) || !edge_fix || e > GK_SP_EMAX)) {
     launch_bt(r2, f2, rund, fund, n, len, e, accept, errc, edge_fix, stream);
     return 0;
   }
   if (!force_generic &&
       dispatch_sp<GK_SP_EMAX>(e, r2, f2, rund, fund, n, len, accept, errc, stream))
-    return 0;
-  if (!force_generic && e <= GK_SPQ_EMAX &&
-      dispatch_spq<GK_SPQ_EMAX>(e, r2, f2, rund, fund, n, len, accept, errc, stream))
     return 0;
   const int64_t tiles = (n + 1023) / 1024;
   int warps = (int)(48 * 1024 / (len * 32 * 4));

@@ -6,9 +6,6 @@
 #ifndef GK_SP_EMAX
 #define GK_SP_EMAX 11  // largest e with an all-register single-pass filter instantiation
 #endif
-#ifndef GK_SPQ_EMAX
-#define GK_SPQ_EMAX 25  // largest e of the shared-memory-Q single-pass instantiations
-#endif
 
 namespace gk {
 
