@@ -126,6 +126,23 @@ int gk_filter_ex(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
                  int64_t n_pairs, int32_t len, int32_t e,
                  uint32_t* d_accept_bits, uint8_t* d_errcount, int32_t flags, void* stream);
 
+/* a2-a6 for EVERY threshold e = 0..e_max in one pass (
+ * the paper sweeps e from 0 to 10% of L).  The final bit-vector
+ * of threshold e is F_e = F_{e-1} & A*D_e & A*I_e, so the
+ * masks of shift k serve every e >= k and one pass over the 2*e_max+1 masks
+ * yields all e_max+1 decisions.  Results are identical to e_max+1 gk_filter
+ * calls (including the Hamming-stage early accept of each e, readings R5/R9).
+ *  d_accept_bits : (e_max+1) rows of gk_result_words(n_pairs) u32, row e =
+ *                  threshold e, bit p%32 of word p/32 (written).
+ *  d_errcount    : (e_max+1) rows of n_pairs bytes, row e (written) or NULL.
+ *  flags         : 0 or GK_FLAG_NO_EDGE_FIX (original GateKeeper).
+ * Same inputs, alignment and ownership as gk_filter.  Errors: GK_ERR_ARG,
+ * GK_ERR_LEN, GK_ERR_E (e_max outside [0, len)), GK_ERR_ALIGN, GK_ERR_CUDA. */
+int gk_filter_sweep(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
+                    const uint32_t* d_read_undef, const uint32_t* d_ref_undef,
+                    int64_t n_pairs, int32_t len, int32_t e_max,
+                    uint32_t* d_accept_bits, uint8_t* d_errcount, int32_t flags, void* stream);
+
 /* a1-a6 in one launch from ASCII (the paper's "device-encoded" kernel, :105):
  * same inputs as two gk_encode calls (reads and refs share `stride`), same
  * outputs as gk_filter; no packed intermediate is written to HBM.

@@ -53,6 +53,7 @@ def load_library(path: str = LIB_PATH):
         "gk_encode": (ctypes.c_int, [P, I64, I32, I64, P, P, P]),
         "gk_filter": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, P]),
         "gk_filter_ex": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, I32, P]),
+        "gk_filter_sweep": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, I32, P]),
         "gk_filter_ascii": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P]),
         "gk_compact_workspace_bytes": (SZ, [I64]),
         "gk_compact": (ctypes.c_int, [P, I64, P, P, P, SZ, P]),
@@ -132,6 +133,24 @@ def filter(reads_packed, refs_packed, read_undef, ref_undef, n: int, length: int
     _check(load_library().gk_filter_ex(_ptr(reads_packed), _ptr(refs_packed), _ptr(read_undef),
                                        _ptr(ref_undef), n, length, e, _ptr(accept),
                                        _ptr(errcount), flags, _stream(stream)), "gk_filter")
+    return accept, errcount
+
+
+def filter_sweep(reads_packed, refs_packed, read_undef, ref_undef, n: int, length: int,
+                 e_max: int, accept=None, errcount=None, want_errcount: bool = True,
+                 flags: int = 0, stream=None):
+    """Every threshold e = 0..e_max in one pass -> (accept bits u32[e_max+1, ceil(n/32)],
+    errcount u8[e_max+1, n] or None); row e equals filter(..., e)."""
+    import torch
+    dev = reads_packed.device
+    rows = e_max + 1
+    if accept is None:
+        accept = torch.empty((rows, max(1, result_words(n))), dtype=torch.int32, device=dev)
+    if errcount is None and want_errcount:
+        errcount = torch.empty((rows, max(1, n)), dtype=torch.uint8, device=dev)
+    _check(load_library().gk_filter_sweep(_ptr(reads_packed), _ptr(refs_packed), _ptr(read_undef),
+                                          _ptr(ref_undef), n, length, e_max, _ptr(accept),
+                                          _ptr(errcount), flags, _stream(stream)), "gk_filter_sweep")
     return accept, errcount
 
 

@@ -100,6 +100,25 @@ int gk_filter(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
                       d_accept_bits, d_errcount, 0, stream);
 }
 
+int gk_filter_sweep(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
+                    const uint32_t* d_read_undef, const uint32_t* d_ref_undef, int64_t n_pairs,
+                    int32_t len, int32_t e_max, uint32_t* d_accept_bits, uint8_t* d_errcount,
+                    int32_t flags, void* stream) {
+  if (n_pairs < 0) return GK_ERR_ARG;
+  if (len < 1 || len > GK_MAX_LEN) return GK_ERR_LEN;
+  if (e_max < 0 || e_max >= len) return GK_ERR_E;
+  if (n_pairs == 0) return GK_OK;
+  if (!d_reads_packed || !d_refs_packed || !d_read_undef || !d_ref_undef || !d_accept_bits)
+    return GK_ERR_ARG;
+  if (!aligned(d_reads_packed, 16) || !aligned(d_refs_packed, 16) || !aligned(d_read_undef, 4) ||
+      !aligned(d_ref_undef, 4) || !aligned(d_accept_bits, 4))
+    return GK_ERR_ALIGN;
+  gk::launch_filter_sweep(d_reads_packed, d_refs_packed, d_read_undef, d_ref_undef, n_pairs, len,
+                          e_max, d_accept_bits, d_errcount, flags & GK_FLAG_NO_EDGE_FIX,
+                          (cudaStream_t)stream);
+  return after_launch();
+}
+
 int gk_filter_ascii(const uint8_t* d_reads, const uint8_t* d_refs, int64_t stride,
                     int64_t n_pairs, int32_t len, int32_t e, uint32_t* d_accept_bits,
                     uint8_t* d_errcount, void* stream) {

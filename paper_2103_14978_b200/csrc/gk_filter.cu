@@ -157,4 +157,16 @@ int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* r
   return 0;
 }
 
+void launch_bt_sweep(const uint2* reads, const uint2* refs, const uint32_t* rund,
+                     const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,
+                     uint8_t* errc, int edge_fix, cudaStream_t stream);
+
+int launch_filter_sweep(const uint32_t* reads, const uint32_t* refs, const uint32_t* rund,
+                        const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,
+                        uint8_t* errc, int flags, cudaStream_t stream) {
+  launch_bt_sweep(reinterpret_cast<const uint2*>(reads), reinterpret_cast<const uint2*>(refs),
+                  rund, fund, n, len, emax, accept, errc, (flags & 2) ? 0 : 1, stream);
+  return 0;
+}
+
 }  // namespace gk

@@ -121,8 +121,10 @@ __device__ __forceinline__ void shifted_mask13(const Win& R, const Ring& Qw, uin
 // holds the words of step k0; qd / qi point at Q[ib-2-k0] / Q[ib+9+k0] of this
 // lane.  Step k loads the words of step k+1 (<= kend+1, in range: block()
 // keeps kend below the first checked step).
+template <class Hook>
 __device__ __forceinline__ void chunk(const uint2* qd, const uint2* qi, const Win& R, Ring& D,
-                                      Ring& I, uint32_t (&F)[B], int k0, int kend) {
+                                      Ring& I, uint32_t (&F)[B], int k0, int kend,
+                                      const Hook& hook) {
 #define GK_BT_STEP(T)                                                                  \
   if (k0 + (T) <= kend) {                                                              \
     const uint2 nd = __ldg(qd - 32 * ((T) + 1));                                       \
@@ -133,6 +135,7 @@ __device__ __forceinline__ void chunk(const uint2* qd, const uint2* qi, const Wi
     I.l[(T) % W1] = ni.y;                                                              \
     shifted_mask13<((T) + 1) % W1, true>(R, D, F);                                     \
     shifted_mask13<((T) + 1) % W1, false>(R, I, F);                                    \
+    hook(k0 + (T), F);                                                                 \
   } else {                                                                             \
     return;                                                                            \
   }
@@ -146,9 +149,10 @@ static_assert(W1 == 13, "chunk() unrolls one full rotation of the 13-slot ring")
 // Steps k = k0..e of an edge block, rolled (compact code): the windows and
 // their source-validity planes shift by register moves (FMA-pipe IMAD.MOV),
 // one new word and one validity word enter per step.
+template <class Hook>
 __device__ __forceinline__ void checked_steps(const uint2* q, const Win& R, const uint32_t (&tv)[W],
                                               uint32_t (&F)[B], int ib, int len, int k0, int e,
-                                              int edge_fix) {
+                                              int edge_fix, const Hook& hook) {
   // windows of step k0-1 in logical layout
   Win D, I;
   uint32_t dv[W], iv[W], vd[B], vi[B];
@@ -202,6 +206,7 @@ __device__ __forceinline__ void checked_steps(const uint2* q, const Win& R, cons
     vi[B - 1] = ef & ones_if_nonneg(ib + B - 1 - len + k);
     shifted_mask_checked(R, D, dv, tv, vd, F);
     shifted_mask_checked(R, I, iv, tv, vi, F);
+    hook(k, F);
   }
 }
 
@@ -220,9 +225,10 @@ __device__ __forceinline__ void count_starts(const uint32_t (&M)[B], uint32_t& p
 // One block [ib, ib+B).  R holds the reference window R[ib-2 .. ib+9] on entry
 // (edge blocks: clamped loads, masked by tv) and R[ib+6 .. ib+17] on exit; the
 // 8 new words of the next window are loaded at entry, a whole block ahead of use.
+template <class Hook>
 __device__ __forceinline__ void block(const uint2* q, const uint2* r, Win& R, int ib, int len,
                                       int e, int edge_fix, CsaCounter& cA, CsaCounter& cF,
-                                      uint32_t& aprev, uint32_t& fprev) {
+                                      uint32_t& aprev, uint32_t& fprev, const Hook& hook) {
   uint2 rn[B];
 #pragma unroll
   for (int d = 0; d < B; ++d) rn[d] = ldc(r, ib + B + 2 + d, len);
@@ -276,7 +282,7 @@ __device__ __forceinline__ void block(const uint2* q, const uint2* r, Win& R, in
   // as the Hamming window (k = 0); the rest run checked
   // (one step short of ku: the ring loads one step ahead and stays in range)
   const int ku = edge_t ? 0 : min(ib - 2, len - ib - B - 2) - 1;
-  const int kend = ku < e ? ku : e;
+  const int kend = max(0, ku < e ? ku : e);  // ku < 0 near the end: all steps checked
   if (kend > 0) {
     Ring D, I;
 #pragma unroll
@@ -295,10 +301,10 @@ __device__ __forceinline__ void block(const uint2* q, const uint2* r, Win& R, in
     }
 #pragma unroll 1
     for (int k0 = 1; k0 <= kend; k0 += W1)
-      chunk(qd - 32 * k0, qi + 32 * k0, R, D, I, F, k0, kend);
+      chunk(qd - 32 * k0, qi + 32 * k0, R, D, I, F, k0, kend, hook);
   }
-  if (kend < e) checked_steps(q, R, tv, F, ib, len, kend + 1, e, edge_fix);
-  count_starts(F, fprev, cF);
+  if (kend < e) checked_steps(q, R, tv, F, ib, len, kend + 1, e, edge_fix, hook);
+  if (!Hook::kSweep) count_starts(F, fprev, cF);
   // slide the reference window by one block
 #pragma unroll
   for (int c = 0; c < W - B; ++c) {
@@ -311,6 +317,46 @@ __device__ __forceinline__ void block(const uint2* q, const uint2* r, Win& R, in
     R.l[W - B + d] = rn[d].y;
   }
 }
+
+// Per-k hooks of block(): called with the block's F words once step k is ANDed
+// in, i.e. with F_k = A0 & AND_{j<=k} (A*D_j & A*I_j).
+struct NoHook {
+  static constexpr bool kSweep = false;
+  __device__ __forceinline__ void operator()(int, const uint32_t (&)[B]) const {}
+};
+
+// Threshold sweep: F_e of every e <= e_max is a prefix
+// of the same AND chain, so one pass counts all of them.  The counter of F_k
+// (8 bit-sliced planes, CsaCounter layout) and its last F word (the run-start
+// carry into the next block) live in shared memory, [k-1][9][32 lanes]:
+// bank = lane, conflict-free.
+struct SweepHook {
+  static constexpr bool kSweep = true;
+  uint32_t* sm;  // this warp's counters, already offset by lane
+  __device__ __forceinline__ void operator()(int k, const uint32_t (&F)[B]) const {
+    uint32_t* p = sm + (k - 1) * 9 * 32;
+    uint32_t prev = p[8 * 32];
+    uint32_t st[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      st[u] = F[u] & ~(prev & notstart_of(u));
+      prev = F[u];
+    }
+    p[8 * 32] = prev;
+    CsaCounter c;
+    c.ones = p[0];
+    c.twos = p[32];
+    c.fours = p[64];
+#pragma unroll
+    for (int b = 0; b < 5; ++b) c.up[b] = p[(3 + b) * 32];
+    c.add8(st);
+    p[0] = c.ones;
+    p[32] = c.twos;
+    p[64] = c.fours;
+#pragma unroll
+    for (int b = 0; b < 5; ++b) p[(3 + b) * 32] = c.up[b];
+  }
+};
 
 }  // namespace bt
 
@@ -337,7 +383,7 @@ __global__ void __launch_bounds__(128, 3) filter_bt_kernel(
   }
 #pragma unroll 1
   for (int ib = 0; ib < len; ib += bt::B) {
-    bt::block(q, r, R, ib, len, e, edge_fix, cA, cF, aprev, fprev);
+    bt::block(q, r, R, ib, len, e, edge_fix, cA, cF, aprev, fprev, bt::NoHook{});
   }
   uint32_t a[8], f[8];
   cA.planes(a);
@@ -355,6 +401,75 @@ void launch_bt(const uint2* reads, const uint2* refs, const uint32_t* rund, cons
   cudaFuncSetAttribute(filter_bt_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
   filter_bt_kernel<<<(unsigned)blocks, warps * 32, 0, stream>>>(reads, refs, rund, fund, n, len, e,
                                                                  accept, errc, edge_fix);
+}
+
+// a2-a6 for every e in [0, e_max] in one pass (gk_filter_sweep): the k loop of
+// each block runs to e_max and the hook counts F_k after every step; the
+// decision for e uses c0 (the Hamming-stage count, readings R5/R9) and count(F_e).
+constexpr int SWEEP_WARPS = 2;
+
+__global__ void __launch_bounds__(SWEEP_WARPS * 32, 6) filter_bt_sweep_kernel(
+    const uint2* __restrict__ reads, const uint2* __restrict__ refs,
+    const uint32_t* __restrict__ rund, const uint32_t* __restrict__ fund, int64_t n, int len,
+    int emax, uint32_t* __restrict__ accept, uint8_t* __restrict__ errc, int edge_fix) {
+  extern __shared__ uint32_t sm_sweep[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t tile = (int64_t)blockIdx.x * SWEEP_WARPS + warp;
+  const int64_t g = tile * 32 + lane;
+  if (tile * 1024 >= n) return;
+  uint32_t* mine = sm_sweep + (size_t)warp * emax * 9 * 32 + lane;
+  for (int j = 0; j < emax * 9; ++j) mine[j * 32] = 0u;
+  const uint2* q = reads + tile * (int64_t)len * 32 + lane;
+  const uint2* r = refs + tile * (int64_t)len * 32 + lane;
+  CsaCounter cA, cF;
+  cA.clear();
+  cF.clear();
+  uint32_t aprev = 0u, fprev = 0u;
+  bt::Win R;
+#pragma unroll
+  for (int c = 0; c < bt::W; ++c) {
+    const uint2 v = bt::ldc(r, c - 2, len);
+    R.h[c] = v.x;
+    R.l[c] = v.y;
+  }
+  const bt::SweepHook hook{mine};
+#pragma unroll 1
+  for (int ib = 0; ib < len; ib += bt::B) {
+    bt::block(q, r, R, ib, len, emax, edge_fix, cA, cF, aprev, fprev, hook);
+  }
+  if (g * 32 >= n) return;
+  uint32_t a[8], f[8];
+  cA.planes(a);
+  const uint32_t und = __ldg(rund + g) | __ldg(fund + g);
+  const int64_t words = (n + 31) / 32;
+#pragma unroll 1
+  for (int e = 0; e <= emax; ++e) {
+    if (e == 0) {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) f[b] = a[b];
+    } else {
+      const uint32_t* p = mine + (e - 1) * 9 * 32;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) f[b] = p[b * 32];
+    }
+    finish_group(a, f, e, und, g, n, accept + e * words, errc ? errc + e * n : nullptr);
+  }
+}
+
+size_t sweep_smem_bytes(int emax) { return (size_t)SWEEP_WARPS * emax * 9 * 32 * 4; }
+
+void launch_bt_sweep(const uint2* reads, const uint2* refs, const uint32_t* rund,
+                     const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,
+                     uint8_t* errc, int edge_fix, cudaStream_t stream) {
+  const int64_t tiles = (n + 1023) / 1024;
+  const int64_t blocks = (tiles + SWEEP_WARPS - 1) / SWEEP_WARPS;
+  const size_t smem = sweep_smem_bytes(emax);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(filter_bt_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  filter_bt_sweep_kernel<<<(unsigned)blocks, SWEEP_WARPS * 32, smem, stream>>>(
+      reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix);
 }
 
 }  // namespace gk

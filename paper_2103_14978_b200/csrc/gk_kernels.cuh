@@ -16,6 +16,10 @@ int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* r
                   const uint32_t* fund, int64_t n, int len, int e, uint32_t* accept,
                   uint8_t* errc, int flags, cudaStream_t stream);
 
+int launch_filter_sweep(const uint32_t* reads, const uint32_t* refs, const uint32_t* rund,
+                        const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,
+                        uint8_t* errc, int flags, cudaStream_t stream);
+
 int launch_filter_ascii(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n,
                         int len, int e, uint32_t* accept, uint8_t* errc, cudaStream_t stream);
 

@@ -27,7 +27,7 @@ def declared_functions():
 
 def test_header_declares_the_boundary():
     names = declared_functions()
-    for must in ["gk_encode", "gk_filter", "gk_filter_ascii", "gk_compact", "gk_filter_host",
+    for must in ["gk_encode", "gk_filter", "gk_filter_ascii", "gk_filter_sweep", "gk_compact", "gk_filter_host",
                  "gk_version", "gk_status_string", "gk_last_cuda_error"]:
         assert must in names
 
@@ -69,6 +69,12 @@ def test_argument_validation_before_any_launch(lib):
     assert lib.gk_filter(P, P, P, P, 0, 100, 2, None, None, None) == 0
     assert lib.gk_filter(None, P, P, P, 10, 100, 2, P, None, None) == -1
     assert lib.gk_filter_ascii(P, P, 100, 10, 100, 100, P, None, None) == -3
+    assert lib.gk_filter_sweep(P, P, P, P, 10, 100, 100, P, None, 0, None) == -3  # e_max >= len
+    assert lib.gk_filter_sweep(P, P, P, P, 10, 100, -1, P, None, 0, None) == -3
+    assert lib.gk_filter_sweep(P, P, P, P, 10, 0, 0, P, None, 0, None) == -2
+    assert lib.gk_filter_sweep(P, P, P, P, 0, 100, 5, None, None, 0, None) == 0
+    assert lib.gk_filter_sweep(P, P, None, P, 10, 100, 5, P, None, 0, None) == -1
+    assert lib.gk_filter_sweep(P + 8, P, P, P, 10, 100, 5, P, None, 0, None) == -4
     assert lib.gk_filter_ascii(P, P, 2000, 10, 100, 2, P, None, None) == -1  # stride limit
     assert lib.gk_compact(P, 10, P, P, P, 0, None) == -5                    # workspace
     assert lib.gk_compact(P, 1 << 33, P, P, P, 1 << 20, None) == -1

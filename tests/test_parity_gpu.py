@@ -185,6 +185,91 @@ def test_no_errcount_output(gk):
     assert (unpack_accept(acc, 3000) == oa).all() and (unpack_accept(acc2, 3000) == oa).all()
 
 
+# ---------------------------------------------------------------- sweep --------
+def run_sweep(gk, reads, refs, emax, L=None, flags=0):
+    n, stride = reads.shape
+    L = stride if L is None else L
+    dr, df = to_dev(reads), to_dev(refs)
+    q, uq = gk.encode(dr, L)
+    r, ur = gk.encode(df, L)
+    acc, err = gk.filter_sweep(q, r, uq, ur, n, L, emax, flags=flags)
+    torch.cuda.synchronize()
+    return [unpack_accept(acc[e], n) for e in range(emax + 1)], err.cpu().numpy()[:, :n]
+
+
+def assert_sweep_parity(gk, reads, refs, emax, L=None, flags=0):
+    a, c = run_sweep(gk, reads, refs, emax, L, flags)
+    if flags & gk.GK_FLAG_NO_EDGE_FIX:
+        ref = [oracle.filter(reads, refs, e, L, edge_fix=False) for e in range(emax + 1)]
+        oa, oc = [x[0] for x in ref], [x[1] for x in ref]
+    else:
+        oa, oc = oracle.sweep(reads, refs, emax, L)
+    for e in range(emax + 1):
+        bad = np.nonzero((a[e] != oa[e]) | (c[e] != oc[e]))[0]
+        assert bad.size == 0, (f"{bad.size} mismatches (L={L}, e={e} of sweep to {emax}, "
+                               f"flags={flags}); first: {bad[:5]}")
+
+
+@pytest.mark.parametrize("L", [100, 150, 250])
+def test_sweep_kernel_paper_profile(gk, L):
+    """gk_filter_sweep (one pass, every e <= e_max) == the oracle's e sweep."""
+    reads, refs = pairgen.gen_pairs(5000, L, seed=pairgen.SEED + 3 * L)
+    assert_sweep_parity(gk, reads, refs, {100: 10, 150: 15, 250: 25}[L])
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 5, 8, 9, 16, 17, 31, 33, 64, 100, 129, 255, 508])
+def test_sweep_kernel_random_lengths(gk, L):
+    n = 1500 if L < 300 else 600
+    reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED,
+                                    emax=max(1, L // 10), seed=L + 7)
+    assert_sweep_parity(gk, reads, refs, min(L - 1, max(L // 10, 13)))
+    if L > 1:
+        assert_sweep_parity(gk, reads, refs, min(L - 1, 3))
+
+
+def test_sweep_kernel_adversarial_and_ragged(gk):
+    L = 48
+    rng = np.random.default_rng(5)
+    base = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, (700, L))]
+    q = base.copy(); q[:, :3] = ord("T")
+    assert_sweep_parity(gk, q, base.copy(), 47)
+    q = np.roll(base, 2, axis=1); q[::5, 20] = ord("N")
+    assert_sweep_parity(gk, q, base.copy(), 20)
+    for n in (1, 33, 1025, 2049):
+        reads, refs = pairgen.gen_pairs(n, 100, profile=pairgen.PROFILE_BALANCED, emax=6, seed=n)
+        assert_sweep_parity(gk, reads, refs, 12)
+
+
+@pytest.mark.parametrize("L", [17, 100])
+def test_sweep_kernel_original_gatekeeper(gk, L):
+    reads, refs = pairgen.gen_pairs(2000, L, profile=pairgen.PROFILE_BALANCED, emax=L // 10 + 1,
+                                    seed=L + 1234)
+    assert_sweep_parity(gk, reads, refs, L // 5, flags=gk.GK_FLAG_NO_EDGE_FIX)
+
+
+def test_sweep_kernel_full_size_sampled(gk):
+    """C2 at full size (30M x 100 bp, e = 0..10) as bench.py --path sweep runs it:
+    every row equals gk_filter at that e; sampled chunks equal the oracle."""
+    n, L, emax = 30_000_000, 100, 10
+    dr, df = pairgen.gen_pairs_cuda(n, L)
+    q, uq = gk.encode(dr, L)
+    r, ur = gk.encode(df, L)
+    del dr, df
+    acc, err = gk.filter_sweep(q, r, uq, ur, n, L, emax)
+    for e in (0, 3, 10):
+        a1, c1 = gk.filter(q, r, uq, ur, n, L, e)
+        assert torch.equal(acc[e], a1) and torch.equal(err[e], c1), e
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(11)
+    for s in sorted(rng.integers(0, n - 4096, size=4).tolist()) + [n - 4096]:
+        s = (s // 32) * 32
+        reads, refs = pairgen.gen_pairs(4096, L, idx0=s)
+        oa, oc = oracle.sweep(reads, refs, emax)
+        for e in range(emax + 1):
+            bits = unpack_accept(acc[e, s // 32:(s + 4096) // 32], 4096)
+            assert (bits == oa[e]).all() and (err[e, s:s + 4096].cpu().numpy() == oc[e]).all(), (s, e)
+
+
 # ---------------------------------------------------------------- compact ------
 @pytest.mark.parametrize("n", [1, 77, 4096, 70_001, 300_000])
 def test_compact_indices(gk, n):

@@ -1,6 +1,6 @@
 """Small invocation of every kernel of libgk.so, for compute-sanitizer runs
 (memcheck / racecheck / synccheck / initcheck): TMA encoder + tail paths, the
-register filter, the large-e warp-pair filter, the mask-major fallback, the fused
+register filter, the block-transposed filter and its e sweep, the mask-major fallback, the fused
 ASCII filter, compaction and the host pipelines."""
 import os
 import sys
@@ -21,6 +21,8 @@ for L, n in [(100, 3000), (150, 2200), (37, 1500)]:
     for e in (0, 3, 13, L - 1 if L < 40 else 30):
         acc, err = gk.filter(q, s, uq, us, n, L, e)
         gk.filter(q, s, uq, us, n, L, e, flags=gk.GK_FLAG_NO_EDGE_FIX)
+        gk.filter(q, s, uq, us, n, L, e, flags=gk.GK_FLAG_GENERIC)
+        gk.filter_sweep(q, s, uq, us, n, L, e)
         gk.filter_ascii(r, f, e, L)
         gk.compact(acc, n)
     torch.cuda.synchronize()
