@@ -52,7 +52,11 @@ def parse():
                    help="c5: total pairs over all ranks (the 100/150/250 bp mix)")
     p.add_argument("--mem-gb", type=float, default=100.0,
                    help="c5: device memory budget for resident inputs per rank")
-    p.add_argument("--path", default="packed", choices=["fused", "packed"])
+    p.add_argument("--path", default="sweep", choices=["sweep", "packed", "fused"],
+                   help="sweep: gk_encode x2 + gk_filter_sweep (all e in one pass); packed: "
+                        "gk_encode x2 + gk_filter per e; fused: gk_filter_ascii per e")
+    p.add_argument("--no-alt", action="store_true",
+                   help="skip the extra timing of the per-e packed path")
     p.add_argument("--n", type=int, default=None, help="override pairs per GPU")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -217,12 +221,14 @@ def main():
     idx0, n = sharding.weak_shard(n, rank)
     reads, refs = pairgen.gen_pairs_cuda(n, L, idx0=idx0, device=dev)
     stream = torch.cuda.current_stream(dev)
-    accept = torch.empty(gk.result_words(n), dtype=torch.int32, device=dev)
-    errc = torch.empty(n, dtype=torch.uint8, device=dev)
+    rows = len(es) if args.path == "sweep" else 1
+    assert es == list(range(len(es)))
+    accept = torch.empty((rows, gk.result_words(n)), dtype=torch.int32, device=dev)
+    errc = torch.empty((rows, n), dtype=torch.uint8, device=dev)
     idx = torch.empty(n, dtype=torch.int32, device=dev)
     n_acc = torch.zeros(len(es), dtype=torch.int64, device=dev)
     ws = torch.empty(gk.compact_workspace_bytes(n), dtype=torch.uint8, device=dev)
-    if args.path == "packed":
+    if args.path in ("packed", "sweep"):
         pq = torch.empty(gk.packed_words(n, L), dtype=torch.int32, device=dev)
         pr = torch.empty_like(pq)
         uq = torch.empty(gk.undef_words(n), dtype=torch.int32, device=dev)
@@ -233,28 +239,45 @@ def main():
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_ev)]
     ev_enc = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     enc_launches = 0
-    if args.path == "packed":
+    if args.path in ("packed", "sweep"):
         enc_launches = 2 * (1 + (1 if n % 128 else 0) + (1 if (n + 1023) // 1024 * 32 > (n + 31) // 32 else 0))
-    launches_per_step = len(es) * 3 + enc_launches
+    if args.path == "sweep":
+        launches_per_step = 1 + len(es) * 2 + enc_launches
+    else:
+        launches_per_step = len(es) * 3 + enc_launches
 
-    def step(record=False):
-        if args.path == "packed":
+    def step(record=False, path=args.path):
+        if path in ("packed", "sweep"):
             if record:
                 ev_enc[0].record(stream)
             gk.encode(reads, L, out=(pq, uq), stream=stream)
             gk.encode(refs, L, out=(pr, ur), stream=stream)
             if record:
                 ev_enc[1].record(stream)
+        if path == "sweep":
+            # a2-a6 for every e in one pass, then a7 per e
+            if record:
+                ev[0][0].record(stream)
+            gk.filter_sweep(pq, pr, uq, ur, n, L, es[-1], accept=accept, errcount=errc,
+                            stream=stream)
+            if record:
+                ev[0][1].record(stream)
+            for j, e in enumerate(es):
+                gk.compact(accept[e], n, idx=idx, n_acc=n_acc[j:j + 1], workspace=ws,
+                           stream=stream)
+            if record:
+                ev[0][2].record(stream)
+            return
         for j, e in enumerate(es):
             if record:
                 ev[j][0].record(stream)
-            if args.path == "fused":
-                gk.filter_ascii(reads, refs, e, L, accept=accept, errcount=errc, stream=stream)
+            if path == "fused":
+                gk.filter_ascii(reads, refs, e, L, accept=accept[0], errcount=errc[0], stream=stream)
             else:
-                gk.filter(pq, pr, uq, ur, n, L, e, accept=accept, errcount=errc, stream=stream)
+                gk.filter(pq, pr, uq, ur, n, L, e, accept=accept[0], errcount=errc[0], stream=stream)
             if record:
                 ev[j][1].record(stream)
-            gk.compact(accept, n, idx=idx, n_acc=n_acc[j:j + 1], workspace=ws, stream=stream)
+            gk.compact(accept[0], n, idx=idx, n_acc=n_acc[j:j + 1], workspace=ws, stream=stream)
             if record:
                 ev[j][2].record(stream)
 
@@ -279,13 +302,32 @@ def main():
     torch.cuda.synchronize(dev)
     clocks = sampler.stop()
     # kernel times of the LAST step's launches (events are reused each step)
-    for j in range(n_ev):
+    n_rec = 1 if args.path == "sweep" else n_ev
+    for j in range(n_rec):
         filt_ms[j] = ev[j][0].elapsed_time(ev[j][1])
         comp_ms[j] = ev[j][1].elapsed_time(ev[j][2])
     elapsed = sharding.max_over_ranks(t_start.elapsed_time(t_end), device=dev)
     n_acc_tot = sharding.sum_over_ranks(n_acc, device=dev)
     if world > 1:
         dist.barrier()
+
+    # the per-e packed path on the same data (context for the sweep's speed-up)
+    alt = None
+    if args.path == "sweep" and not args.no_alt:
+        for _ in range(2):
+            step(path="packed")
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        a0.record(stream)
+        for _ in range(3):
+            step(path="packed")
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        alt_ms = sharding.max_over_ranks(a0.elapsed_time(a1) / 3, device=dev)
+        alt = {"path": "gk_encode x2 + (gk_filter + gk_compact) per e", "steps": 3,
+               "ms_per_step": round(alt_ms, 4),
+               "value": round(n * len(es) * world / (alt_ms / 1e3) / 1e9, 4)}
 
     ms_per_step = elapsed / args.steps
     filtrations = n * len(es) * world
@@ -295,7 +337,7 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 64 * clk_mhz * 1e6 / 1e12  # T int-ops/s: 148 SMs x 4 SMSPs x 16 ALU lanes
-    enc_ms = ev_enc[0].elapsed_time(ev_enc[1]) if args.path == "packed" else 0.0
+    enc_ms = ev_enc[0].elapsed_time(ev_enc[1]) if args.path in ("packed", "sweep") else 0.0
 
     def alg_ops(e):
         # method-minimum integer ops per pair on bit-sliced words:
@@ -303,15 +345,27 @@ def main():
         cells = L * (2 * e + 1) - e * (e + 1)
         return (5 * cells + 8 * L) / 32.0
 
+    def sweep_ops(emax):
+        # one pass: the 2*emax+1 masks once + one window counter per e (4 ops per position)
+        cells = L * (2 * emax + 1) - emax * (emax + 1)
+        return (5 * cells + 4 * L * (emax + 2)) / 32.0
+
     if args.path == "fused":
         bytes_launch = n * (2 * L) + n / 8 + n
         kname = "gk_filter_ascii (filter_ascii_kernel)"
+    elif args.path == "sweep":
+        bytes_launch = n * (L / 2) + (n / 8 + n) * n_ev
+        kname = "gk_filter_sweep (filter_bt_sweep_kernel)"
     else:
         bytes_launch = n * (L / 2) + n / 8 + n
-        kname = "gk_filter (filter_sp_kernel<E> / filter_generic_kernel)"
+        kname = "gk_filter (filter_sp_kernel<E> / filter_bt_kernel)"
     tot_ms = sum(filt_ms)
-    hbm_ach = bytes_launch * n_ev / (tot_ms / 1e3) / 1e9
-    alu_ach = sum(n * alg_ops(e) for e in es) / (tot_ms / 1e3) / 1e12
+    n_launch = n_rec
+    hbm_ach = bytes_launch * n_launch / (tot_ms / 1e3) / 1e9
+    if args.path == "sweep":
+        alu_ach = n * sweep_ops(es[-1]) / (tot_ms / 1e3) / 1e12
+    else:
+        alu_ach = sum(n * alg_ops(e) for e in es) / (tot_ms / 1e3) / 1e12
     if args.path == "fused":
         roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(hbm_ach / hbm_peak, 4)}
@@ -324,18 +378,25 @@ def main():
     roof.update({"kernel": kname, "traffic": None, "peak_source": peak_src,
                  "alu_peak_basis": f"148 SM x 64 ALU lanes/clk x {clk_mhz:.0f} MHz (B200_PROFILING.md / B300_MICROARCH.md)",
                  "hbm_frac": round(hbm_ach / hbm_peak, 4), "alu_frac": round(alu_ach / alu_peak, 4),
-                 "bytes_per_launch": bytes_launch, "mean_launch_ms": round(tot_ms / n_ev, 4),
+                 "bytes_per_launch": bytes_launch, "mean_launch_ms": round(tot_ms / n_launch, 4),
+                 "ops_per_pair": round(sweep_ops(es[-1]) if args.path == "sweep" else
+                                       sum(alg_ops(e) for e in es) / n_ev, 2),
                  "share_of_step": round(tot_ms / ms_per_step, 4)})
     per_e = {}
     for j, e in enumerate(es):
+        if args.path == "sweep":
+            per_e[str(e)] = {"accepted": int(n_acc_tot[j])}
+            continue
         t = filt_ms[j] / 1e3
         per_e[str(e)] = {"filter_ms": round(filt_ms[j], 4), "compact_ms": round(comp_ms[j], 4),
                          "Gpairs_s_filter": round(n / t / 1e9, 3),
                          "hbm_frac": round(bytes_launch / t / 1e9 / hbm_peak, 4),
                          "alu_frac": round(n * alg_ops(e) / t / 1e12 / alu_peak, 4),
                          "accepted": int(n_acc_tot[j])}
+    if args.path == "sweep":
+        per_e["compact_ms_all_e"] = round(comp_ms[0], 4)
     encode = None
-    if args.path == "packed":
+    if args.path in ("packed", "sweep"):
         enc_bytes = 2 * (n * L + n * L / 4 + n / 8)
         encode = {"ms": round(enc_ms, 4), "GB_s": round(enc_bytes / (enc_ms / 1e3) / 1e9, 1),
                   "hbm_frac": round(enc_bytes / (enc_ms / 1e3) / 1e9 / hbm_peak, 4),
@@ -357,16 +418,20 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {
                 "workload": f"{args.config}: {n} pairs x {L} bp per GPU, e swept {es[0]}..{es[-1]} "
-                            f"(BASELINE configs[{cidx}]); step = per e: a1-a6 + a7",
+                            f"(BASELINE configs[{cidx}]); step = "
+                            + ("a1 once, a2-a6 for all e in one pass, a7 per e" if args.path == "sweep"
+                               else "per e: a1-a6 + a7"),
                 "n_pairs_per_gpu": n, "read_len": L, "e": f"{es[0]}-{es[-1]}",
-                "path": "gk_filter_ascii + gk_compact" if args.path == "fused"
-                        else "gk_encode x2 + gk_filter + gk_compact",
+                "path": {"fused": "gk_filter_ascii + gk_compact per e",
+                         "packed": "gk_encode x2 + (gk_filter + gk_compact) per e",
+                         "sweep": "gk_encode x2 + gk_filter_sweep + gk_compact per e"}[args.path],
                 "profile": "paper", "seed": BASE_SEED,
                 "l2": f"inputs {2 * n * L / 1e9:.1f} GB per GPU > 126 MB L2 (no flush needed)",
                 "parallelism": f"dp{world} (pairs sharded, no data-path collective)"},
             "roofline": roof,
             "encode": encode,
             "per_e": per_e,
+            "alt_path": alt,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "e2e": e2e,
@@ -474,7 +539,7 @@ def measure_e2e(gk, torch, dev, n, L, es, rank, world, args):
     acc = torch.empty((len(es), gk.result_words(n_e2e)), dtype=torch.int32, pin_memory=True)
     err = torch.empty((len(es), n_e2e), dtype=torch.uint8, pin_memory=True)
     chunk = 1 << 21
-    ws = torch.empty(gk.host_sweep_workspace_bytes(chunk, L, L, len(es)), dtype=torch.uint8,
+    ws = torch.empty(gk.host_sweep_workspace_bytes(chunk, L, L, max(es)), dtype=torch.uint8,
                      device=dev)
     torch.cuda.synchronize(dev)
 
@@ -501,7 +566,7 @@ def measure_e2e(gk, torch, dev, n, L, es, rank, world, args):
             "h2d_bytes_per_step": 2 * n_e2e * L,
             "d2h_bytes_per_step": (n_e2e // 8 + n_e2e) * len(es),
             "api": "gk_filter_host_sweep (pinned host buffers; each chunk copied + encoded once, "
-                   "filtered for every e; 2-stream pipeline)",
+                   "filtered for every e in one gk_filter_sweep pass; 2-stream pipeline)",
             "n_pairs_per_gpu": n_e2e, "timer": "host wall clock around the synchronous call"}
 
 

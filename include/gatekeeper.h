@@ -181,14 +181,16 @@ int gk_filter_host(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride
                    void* d_ws, size_t ws_bytes, int64_t chunk_pairs);
 
 /* Threshold sweep from HOST buffers: every chunk of pairs crosses PCIe and is
- * encoded once, then filtered for each of the n_e thresholds in e_list (the
- * paper sweeps e from 0 to 10% of L).
+ * encoded once, then filtered for every e <= e_max = max(e_list) in one pass
+ * (gk_filter_sweep; the paper sweeps e from 0 to 10% of L), and
+ * the rows of the requested thresholds are copied back.
  *  e_list          : n_e thresholds (host array), each 0 <= e < len.
  *  h_accept_bits   : n_e * gk_result_words(n_pairs) u32, row t = e_list[t] (written).
  *  h_errcount      : n_e * n_pairs bytes, row t = e_list[t] (written) or NULL.
- *  d_ws            : gk_host_sweep_workspace_bytes(chunk_pairs, stride, len, n_e) bytes.
+ *  d_ws            : gk_host_sweep_workspace_bytes(chunk_pairs, stride, len, e_max)
+ *                    bytes (e_max = the largest threshold of e_list).
  * Synchronous.  Errors: as gk_filter_host. */
-size_t gk_host_sweep_workspace_bytes(int64_t chunk_pairs, int64_t stride, int32_t len, int32_t n_e);
+size_t gk_host_sweep_workspace_bytes(int64_t chunk_pairs, int64_t stride, int32_t len, int32_t e_max);
 int gk_filter_host_sweep(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride,
                          int64_t n_pairs, int32_t len, const int32_t* e_list, int32_t n_e,
                          uint32_t* h_accept_bits, uint8_t* h_errcount,

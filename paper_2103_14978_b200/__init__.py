@@ -216,14 +216,14 @@ def filter_host(reads, refs, e: int, length: int | None = None, accept=None, err
     return accept, errcount
 
 
-def host_sweep_workspace_bytes(chunk_pairs: int, stride: int, length: int, n_e: int) -> int:
-    return load_library().gk_host_sweep_workspace_bytes(chunk_pairs, stride, length, n_e)
+def host_sweep_workspace_bytes(chunk_pairs: int, stride: int, length: int, e_max: int) -> int:
+    return load_library().gk_host_sweep_workspace_bytes(chunk_pairs, stride, length, e_max)
 
 
 def filter_host_sweep(reads, refs, e_list, length: int | None = None, accept=None,
                       errcount=None, workspace=None, chunk_pairs: int = 1 << 20):
     """Threshold sweep of HOST uint8 tensors: each chunk is copied and encoded once, then
-    filtered for every e.  Returns (accept bits [n_e, words], errcount [n_e, n] or None)."""
+    filtered for every e <= max(e_list) in one pass.  Returns (accept bits [n_e, words], errcount [n_e, n] or None)."""
     import torch
     n, stride = reads.shape
     length = stride if length is None else length
@@ -233,7 +233,7 @@ def filter_host_sweep(reads, refs, e_list, length: int | None = None, accept=Non
                              pin_memory=True)
     if workspace is None:
         workspace = torch.empty(host_sweep_workspace_bytes(chunk_pairs, stride, length,
-                                                           len(e_list)),
+                                                           max(e_list)),
                                 dtype=torch.uint8, device="cuda")
     _check(load_library().gk_filter_host_sweep(reads.data_ptr(), refs.data_ptr(), stride, n,
                                                length, es, len(e_list), accept.data_ptr(),

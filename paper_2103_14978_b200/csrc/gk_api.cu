@@ -229,21 +229,21 @@ struct SweepLayout {
   size_t in, packed, undef, acc, err, per_set;
 };
 
-static SweepLayout sweep_layout(int64_t chunk, int64_t stride, int32_t len, int32_t n_e) {
+static SweepLayout sweep_layout(int64_t chunk, int64_t stride, int32_t len, int32_t e_max) {
   SweepLayout L;
   L.in = round_up((size_t)chunk * (size_t)stride, 256);
   L.packed = round_up(gk_packed_words(chunk, len) * 4, 256);
   L.undef = round_up(gk_undef_words(chunk) * 4, 256);
-  L.acc = round_up((size_t)(chunk / 32 + 1) * 4, 256);
+  L.acc = round_up((size_t)(chunk / 32) * 4, 256);  // chunk is a multiple of 1024
   L.err = round_up((size_t)chunk, 256);
-  L.per_set = 2 * L.in + 2 * L.packed + 2 * L.undef + (size_t)n_e * (L.acc + L.err);
+  L.per_set = 2 * L.in + 2 * L.packed + 2 * L.undef + (size_t)(e_max + 1) * (L.acc + L.err);
   return L;
 }
 
 size_t gk_host_sweep_workspace_bytes(int64_t chunk_pairs, int64_t stride, int32_t len,
-                                     int32_t n_e) {
-  if (chunk_pairs <= 0 || stride <= 0 || len <= 0 || n_e <= 0) return 0;
-  return 2 * sweep_layout(chunk_pairs, stride, len, n_e).per_set;
+                                     int32_t e_max) {
+  if (chunk_pairs <= 0 || stride <= 0 || len <= 0 || e_max < 0) return 0;
+  return 2 * sweep_layout(chunk_pairs, stride, len, e_max).per_set;
 }
 
 int gk_filter_host_sweep(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride,
@@ -258,10 +258,12 @@ int gk_filter_host_sweep(const uint8_t* h_reads, const uint8_t* h_refs, int64_t 
   if (n_pairs == 0) return GK_OK;
   if (!h_refs || !h_accept_bits) return GK_ERR_ARG;
   if (chunk_pairs <= 0 || chunk_pairs % 1024 != 0) return GK_ERR_ARG;
-  if (!d_ws || ws_bytes < gk_host_sweep_workspace_bytes(chunk_pairs, stride, len, n_e))
+  int32_t e_max = 0;
+  for (int t = 0; t < n_e; ++t) e_max = e_list[t] > e_max ? e_list[t] : e_max;
+  if (!d_ws || ws_bytes < gk_host_sweep_workspace_bytes(chunk_pairs, stride, len, e_max))
     return GK_ERR_WORKSPACE;
   if (!aligned(d_ws, 256)) return GK_ERR_ALIGN;
-  const SweepLayout L = sweep_layout(chunk_pairs, stride, len, n_e);
+  const SweepLayout L = sweep_layout(chunk_pairs, stride, len, e_max);
   const size_t words_total = gk_result_words(n_pairs);
   cudaStream_t st[2];
   for (int b = 0; b < 2; ++b) {
@@ -293,17 +295,20 @@ int gk_filter_host_sweep(const uint8_t* h_reads, const uint8_t* h_refs, int64_t 
     if (err != cudaSuccess) { rc = cuda_status(err); break; }
     gk::launch_encode(dr, np, len, stride, pq, uq, st[b]);
     gk::launch_encode(df, np, len, stride, pr, ur, st[b]);
+    // every e <= e_max in one pass (gk_filter_sweep); rows of the chunk: [e][chunk/32] bits,
+    // then [e][chunk] counts
+    uint32_t* acc = reinterpret_cast<uint32_t*>(outs);
+    uint8_t* ec = h_errcount ? outs + (size_t)(e_max + 1) * L.acc : nullptr;
+    gk::launch_filter_sweep(pq, pr, uq, ur, np, len, e_max, acc, ec, 0, st[b]);
+    rc = after_launch();
+    const size_t words = (size_t)((np + 31) / 32);
     for (int t = 0; t < n_e && rc == GK_OK; ++t) {
-      uint32_t* acc = reinterpret_cast<uint32_t*>(outs + (size_t)t * (L.acc + L.err));
-      uint8_t* ec = h_errcount ? reinterpret_cast<uint8_t*>(acc) + L.acc : nullptr;
-      gk::launch_filter(pq, pr, uq, ur, np, len, e_list[t], acc, ec, 0, st[b]);
-      rc = after_launch();
-      if (rc) break;
-      err = cudaMemcpyAsync(h_accept_bits + (size_t)t * words_total + p0 / 32, acc,
-                            (size_t)((np + 31) / 32) * 4, cudaMemcpyDeviceToHost, st[b]);
+      const int e = e_list[t];
+      err = cudaMemcpyAsync(h_accept_bits + (size_t)t * words_total + p0 / 32,
+                            acc + (size_t)e * words, words * 4, cudaMemcpyDeviceToHost, st[b]);
       if (err == cudaSuccess && h_errcount)
-        err = cudaMemcpyAsync(h_errcount + (size_t)t * n_pairs + p0, ec, (size_t)np,
-                              cudaMemcpyDeviceToHost, st[b]);
+        err = cudaMemcpyAsync(h_errcount + (size_t)t * n_pairs + p0, ec + (size_t)e * np,
+                              (size_t)np, cudaMemcpyDeviceToHost, st[b]);
       if (err != cudaSuccess) rc = cuda_status(err);
     }
   }

@@ -327,34 +327,43 @@ struct NoHook {
 
 // Threshold sweep: F_e of every e <= e_max is a prefix
 // of the same AND chain, so one pass counts all of them.  The counter of F_k
-// (8 bit-sliced planes, CsaCounter layout) and its last F word (the run-start
-// carry into the next block) live in shared memory, [k-1][9][32 lanes]:
-// bank = lane, conflict-free.
+// (8 bit-sliced planes, CsaCounter layout) lives in shared memory,
+// [k-1][8][32 lanes]: bank = lane, conflict-free.
+// Out of line: the 13-step unrolled chunk would otherwise carry 13 copies of
+// the counting code (instruction-cache pressure, measured: stall_no_instruction).
+__device__ __noinline__ void sweep_count(uint32_t* p, uint32_t f0, uint32_t f1, uint32_t f2,
+                                         uint32_t f3, uint32_t f4, uint32_t f5, uint32_t f6,
+                                         uint32_t f7) {
+  // windows start at positions ib and ib+4 (ib % 8 == 0): run starts never
+  // depend on the previous block (R6, R7)
+  uint32_t st[B];
+  st[0] = f0;
+  st[1] = f1 & ~f0;
+  st[2] = f2 & ~f1;
+  st[3] = f3 & ~f2;
+  st[4] = f4;
+  st[5] = f5 & ~f4;
+  st[6] = f6 & ~f5;
+  st[7] = f7 & ~f6;
+  CsaCounter c;
+  c.ones = p[0];
+  c.twos = p[32];
+  c.fours = p[64];
+#pragma unroll
+  for (int b = 0; b < 5; ++b) c.up[b] = p[(3 + b) * 32];
+  c.add8(st);
+  p[0] = c.ones;
+  p[32] = c.twos;
+  p[64] = c.fours;
+#pragma unroll
+  for (int b = 0; b < 5; ++b) p[(3 + b) * 32] = c.up[b];
+}
+
 struct SweepHook {
   static constexpr bool kSweep = true;
   uint32_t* sm;  // this warp's counters, already offset by lane
   __device__ __forceinline__ void operator()(int k, const uint32_t (&F)[B]) const {
-    uint32_t* p = sm + (k - 1) * 9 * 32;
-    uint32_t prev = p[8 * 32];
-    uint32_t st[B];
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-      st[u] = F[u] & ~(prev & notstart_of(u));
-      prev = F[u];
-    }
-    p[8 * 32] = prev;
-    CsaCounter c;
-    c.ones = p[0];
-    c.twos = p[32];
-    c.fours = p[64];
-#pragma unroll
-    for (int b = 0; b < 5; ++b) c.up[b] = p[(3 + b) * 32];
-    c.add8(st);
-    p[0] = c.ones;
-    p[32] = c.twos;
-    p[64] = c.fours;
-#pragma unroll
-    for (int b = 0; b < 5; ++b) p[(3 + b) * 32] = c.up[b];
+    sweep_count(sm + (k - 1) * 8 * 32, F[0], F[1], F[2], F[3], F[4], F[5], F[6], F[7]);
   }
 };
 
@@ -418,8 +427,8 @@ __global__ void __launch_bounds__(SWEEP_WARPS * 32, 6) filter_bt_sweep_kernel(
   const int64_t tile = (int64_t)blockIdx.x * SWEEP_WARPS + warp;
   const int64_t g = tile * 32 + lane;
   if (tile * 1024 >= n) return;
-  uint32_t* mine = sm_sweep + (size_t)warp * emax * 9 * 32 + lane;
-  for (int j = 0; j < emax * 9; ++j) mine[j * 32] = 0u;
+  uint32_t* mine = sm_sweep + (size_t)warp * emax * 8 * 32 + lane;
+  for (int j = 0; j < emax * 8; ++j) mine[j * 32] = 0u;
   const uint2* q = reads + tile * (int64_t)len * 32 + lane;
   const uint2* r = refs + tile * (int64_t)len * 32 + lane;
   CsaCounter cA, cF;
@@ -449,7 +458,7 @@ __global__ void __launch_bounds__(SWEEP_WARPS * 32, 6) filter_bt_sweep_kernel(
 #pragma unroll
       for (int b = 0; b < 8; ++b) f[b] = a[b];
     } else {
-      const uint32_t* p = mine + (e - 1) * 9 * 32;
+      const uint32_t* p = mine + (e - 1) * 8 * 32;
 #pragma unroll
       for (int b = 0; b < 8; ++b) f[b] = p[b * 32];
     }
@@ -457,7 +466,7 @@ __global__ void __launch_bounds__(SWEEP_WARPS * 32, 6) filter_bt_sweep_kernel(
   }
 }
 
-size_t sweep_smem_bytes(int emax) { return (size_t)SWEEP_WARPS * emax * 9 * 32 * 4; }
+size_t sweep_smem_bytes(int emax) { return (size_t)SWEEP_WARPS * emax * 8 * 32 * 4; }
 
 void launch_bt_sweep(const uint2* reads, const uint2* refs, const uint32_t* rund,
                      const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,

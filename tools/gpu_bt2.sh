@@ -1,0 +1,12 @@
+#!/bin/bash
+set -u
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_parity_gpu.py -q -x -k "sweep or random_lengths or adversarial or ragged or original or paper_profile" > gpurun_out/pytest_bt2.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_bt2.log
+tail -n 3 gpurun_out/pytest_bt2.log
+timeout 600 python tools/cmp_filters.py --L 100 --e 10 --flags 0 4 > gpurun_out/cmp_bt2.jsonl 2>&1
+timeout 600 python tools/cmp_filters.py --L 150 --e 12 15 --flags 4 >> gpurun_out/cmp_bt2.jsonl 2>&1
+timeout 600 python tools/cmp_filters.py --L 250 --e 12 18 25 --flags 4 >> gpurun_out/cmp_bt2.jsonl 2>&1
+timeout 600 python tools/cmp_sweep.py --L 100 --emax 10 >> gpurun_out/cmp_bt2.jsonl 2>&1
+timeout 600 python tools/cmp_sweep.py --L 150 --emax 15 >> gpurun_out/cmp_bt2.jsonl 2>&1
+timeout 600 python tools/cmp_sweep.py --L 250 --emax 25 >> gpurun_out/cmp_bt2.jsonl 2>&1
+cat gpurun_out/cmp_bt2.jsonl
