@@ -228,6 +228,11 @@ def main():
     idx = torch.empty(n, dtype=torch.int32, device=dev)
     n_acc = torch.zeros(len(es), dtype=torch.int64, device=dev)
     ws = torch.empty(gk.compact_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    if args.path == "sweep":
+        # a7 for every row in one launch pair: one index list per e
+        idx_rows = torch.empty((rows, n), dtype=torch.int32, device=dev)
+        ws_rows = torch.empty(gk.compact_rows_workspace_bytes(n, rows), dtype=torch.uint8,
+                              device=dev)
     if args.path in ("packed", "sweep"):
         pq = torch.empty(gk.packed_words(n, L), dtype=torch.int32, device=dev)
         pr = torch.empty_like(pq)
@@ -242,7 +247,7 @@ def main():
     if args.path in ("packed", "sweep"):
         enc_launches = 2 * (1 + (1 if n % 128 else 0) + (1 if (n + 1023) // 1024 * 32 > (n + 31) // 32 else 0))
     if args.path == "sweep":
-        launches_per_step = 1 + len(es) * 2 + enc_launches
+        launches_per_step = 1 + 2 + enc_launches
     else:
         launches_per_step = len(es) * 3 + enc_launches
 
@@ -262,9 +267,8 @@ def main():
                             stream=stream)
             if record:
                 ev[0][1].record(stream)
-            for j, e in enumerate(es):
-                gk.compact(accept[e], n, idx=idx, n_acc=n_acc[j:j + 1], workspace=ws,
-                           stream=stream)
+            gk.compact_rows(accept, n, idx=idx_rows, n_acc=n_acc, workspace=ws_rows,
+                            stream=stream)
             if record:
                 ev[0][2].record(stream)
             return
@@ -424,7 +428,7 @@ def main():
                 "n_pairs_per_gpu": n, "read_len": L, "e": f"{es[0]}-{es[-1]}",
                 "path": {"fused": "gk_filter_ascii + gk_compact per e",
                          "packed": "gk_encode x2 + (gk_filter + gk_compact) per e",
-                         "sweep": "gk_encode x2 + gk_filter_sweep + gk_compact per e"}[args.path],
+                         "sweep": "gk_encode x2 + gk_filter_sweep + gk_compact_rows (all e)"}[args.path],
                 "profile": "paper", "seed": BASE_SEED,
                 "l2": f"inputs {2 * n * L / 1e9:.1f} GB per GPU > 126 MB L2 (no flush needed)",
                 "parallelism": f"dp{world} (pairs sharded, no data-path collective)"},

@@ -163,6 +163,18 @@ size_t gk_compact_workspace_bytes(int64_t n_pairs);
 int gk_compact(const uint32_t* d_accept_bits, int64_t n_pairs, uint32_t* d_idx,
                uint64_t* d_n_acc, void* d_ws, size_t ws_bytes, void* stream);
 
+/* a7 for a batch of rows at once (e.g. the e_max+1 rows of gk_filter_sweep):
+ * row r of accept bits at d_accept_bits + r*bits_row_stride (u32 words, >=
+ * gk_result_words(n_pairs) when n_rows > 1), its indices at d_idx +
+ * r*idx_row_stride (u32, >= n_pairs when n_rows > 1; d_idx may be NULL to only
+ * count), its count at d_n_acc[r].  One launch pair for all rows.
+ *  d_ws : gk_compact_rows_workspace_bytes(n_pairs, n_rows) bytes of scratch.
+ * Errors: as gk_compact (0 <= n_rows <= 65535). */
+size_t gk_compact_rows_workspace_bytes(int64_t n_pairs, int32_t n_rows);
+int gk_compact_rows(const uint32_t* d_accept_bits, int32_t n_rows, int64_t bits_row_stride,
+                    int64_t n_pairs, uint32_t* d_idx, int64_t idx_row_stride, uint64_t* d_n_acc,
+                    void* d_ws, size_t ws_bytes, void* stream);
+
 /* End-to-end from HOST buffers (the paper's "filter time"): streams
  * the pairs through device memory in chunks, overlapping host->device copies,
  * filtering and device->host copies on two CUDA streams.

@@ -57,6 +57,8 @@ def load_library(path: str = LIB_PATH):
         "gk_filter_ascii": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P]),
         "gk_compact_workspace_bytes": (SZ, [I64]),
         "gk_compact": (ctypes.c_int, [P, I64, P, P, P, SZ, P]),
+        "gk_compact_rows_workspace_bytes": (SZ, [I64, I32]),
+        "gk_compact_rows": (ctypes.c_int, [P, I32, I64, I64, P, I64, P, P, SZ, P]),
         "gk_host_workspace_bytes": (SZ, [I64, I64]),
         "gk_filter_host": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P, SZ, I64]),
         "gk_host_sweep_workspace_bytes": (SZ, [I64, I64, I32, I32]),
@@ -190,6 +192,31 @@ def compact(accept, n: int, idx=None, n_acc=None, workspace=None, want_indices: 
     _check(load_library().gk_compact(accept.data_ptr(), n, _ptr(idx), n_acc.data_ptr(),
                                      workspace.data_ptr(), workspace.numel(), _stream(stream)),
            "gk_compact")
+    return idx, n_acc
+
+
+def compact_rows_workspace_bytes(n: int, rows: int) -> int:
+    return load_library().gk_compact_rows_workspace_bytes(n, rows)
+
+
+def compact_rows(accept, n: int, idx=None, n_acc=None, workspace=None, want_indices: bool = True,
+                 stream=None):
+    """a7 for every row of a 2-D accept tensor [rows, >= ceil(n/32)] (e.g. filter_sweep's)
+    in one launch pair -> (idx u32 [rows, n] or None, n_acc i64 [rows])."""
+    import torch
+    rows = accept.shape[0]
+    dev = accept.device
+    if idx is None and want_indices:
+        idx = torch.empty((rows, max(1, n)), dtype=torch.int32, device=dev)
+    if n_acc is None:
+        n_acc = torch.empty(rows, dtype=torch.int64, device=dev)
+    if workspace is None:
+        workspace = torch.empty(max(1, compact_rows_workspace_bytes(n, rows)), dtype=torch.uint8,
+                                device=dev)
+    _check(load_library().gk_compact_rows(accept.data_ptr(), rows, accept.stride(0), n, _ptr(idx),
+                                          idx.stride(0) if idx is not None else 0, n_acc.data_ptr(),
+                                          workspace.data_ptr(), workspace.numel(),
+                                          _stream(stream)), "gk_compact_rows")
     return idx, n_acc
 
 

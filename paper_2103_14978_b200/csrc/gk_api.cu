@@ -151,6 +151,30 @@ int gk_compact(const uint32_t* d_accept_bits, int64_t n_pairs, uint32_t* d_idx,
   return after_launch();
 }
 
+size_t gk_compact_rows_workspace_bytes(int64_t n_pairs, int32_t n_rows) {
+  return gk::compact_workspace_bytes(n_pairs < 0 ? 0 : n_pairs, n_rows < 1 ? 1 : n_rows);
+}
+
+int gk_compact_rows(const uint32_t* d_accept_bits, int32_t n_rows, int64_t bits_row_stride,
+                    int64_t n_pairs, uint32_t* d_idx, int64_t idx_row_stride, uint64_t* d_n_acc,
+                    void* d_ws, size_t ws_bytes, void* stream) {
+  if (n_pairs < 0 || n_pairs >= ((int64_t)1 << 32) || n_rows < 0 || n_rows > 65535)
+    return GK_ERR_ARG;
+  if (n_rows == 0) return GK_OK;
+  if (!d_n_acc) return GK_ERR_ARG;
+  if (!aligned(d_n_acc, 8)) return GK_ERR_ALIGN;
+  if (n_pairs == 0)
+    return cuda_status(cudaMemsetAsync(d_n_acc, 0, 8 * (size_t)n_rows, (cudaStream_t)stream));
+  if (!d_accept_bits) return GK_ERR_ARG;
+  if (n_rows > 1 && bits_row_stride < (int64_t)gk_result_words(n_pairs)) return GK_ERR_ARG;
+  if (d_idx && n_rows > 1 && idx_row_stride < n_pairs) return GK_ERR_ARG;
+  if (!aligned(d_accept_bits, 4) || (d_idx && !aligned(d_idx, 4))) return GK_ERR_ALIGN;
+  if (!d_ws || ws_bytes < gk::compact_workspace_bytes(n_pairs, n_rows)) return GK_ERR_WORKSPACE;
+  gk::launch_compact(d_accept_bits, n_pairs, d_idx, d_n_acc, d_ws, (cudaStream_t)stream, n_rows,
+                     bits_row_stride, idx_row_stride);
+  return after_launch();
+}
+
 // ---- host-buffer end-to-end pipeline ------------------------------------------
 static size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

@@ -50,10 +50,15 @@ __device__ __forceinline__ uint32_t load_word(const uint32_t* bits, int64_t w, i
   return v;
 }
 
+// blockIdx.y = row of a batch (gk_compact_rows): rows of accept bits at
+// bits + y * bstride, counts at cta_counts + y * gridDim.x.
 __global__ void __launch_bounds__(CP_THREADS) compact_count_kernel(const uint32_t* __restrict__ bits,
                                                                    int64_t n,
-                                                                   uint32_t* __restrict__ cta_counts) {
+                                                                   uint32_t* __restrict__ cta_counts,
+                                                                   int64_t bstride) {
   __shared__ uint32_t sm[CP_THREADS / 32];
+  bits += blockIdx.y * bstride;
+  cta_counts += (size_t)blockIdx.y * gridDim.x;
   const int64_t nwords = (n + 31) / 32;
   const int64_t w0 = (int64_t)blockIdx.x * CP_WORDS_PER_CTA + threadIdx.x;
   uint32_t c = 0u;
@@ -67,7 +72,12 @@ __global__ void __launch_bounds__(CP_THREADS) compact_count_kernel(const uint32_
 
 __global__ void __launch_bounds__(CP_THREADS) compact_write_kernel(
     const uint32_t* __restrict__ bits, int64_t n, const uint32_t* __restrict__ cta_counts,
-    uint32_t* __restrict__ idx, unsigned long long* __restrict__ n_acc) {
+    uint32_t* __restrict__ idx, unsigned long long* __restrict__ n_acc, int64_t bstride,
+    int64_t istride) {
+  bits += blockIdx.y * bstride;
+  cta_counts += (size_t)blockIdx.y * gridDim.x;
+  if (idx != nullptr) idx += blockIdx.y * istride;
+  n_acc += blockIdx.y;
   // CTA: 8 warps x 256 consecutive words.  Warp offsets come from a block scan of
   // the warps' popcounts; inside a warp the words are visited in order and lane j
   // writes the index of bit j, so each word's accepted pairs are one contiguous,
@@ -118,20 +128,22 @@ __global__ void __launch_bounds__(CP_THREADS) compact_write_kernel(
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *n_acc = sm_base + total;
 }
 
-size_t compact_workspace_bytes(int64_t n) {
+size_t compact_workspace_bytes(int64_t n, int rows) {
   const int64_t nwords = (n + 31) / 32;
   const int64_t ctas = (nwords + CP_WORDS_PER_CTA - 1) / CP_WORDS_PER_CTA;
-  return (size_t)(ctas > 0 ? ctas : 1) * sizeof(uint32_t);
+  return (size_t)(ctas > 0 ? ctas : 1) * (size_t)(rows > 0 ? rows : 1) * sizeof(uint32_t);
 }
 
+// rows x ceil(n/65536) CTAs per kernel: one launch pair for a whole batch of rows
 int launch_compact(const uint32_t* bits, int64_t n, uint32_t* idx, uint64_t* n_acc, void* ws,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, int rows, int64_t bstride, int64_t istride) {
   const int64_t nwords = (n + 31) / 32;
   const int64_t ctas = (nwords + CP_WORDS_PER_CTA - 1) / CP_WORDS_PER_CTA;
   uint32_t* counts = reinterpret_cast<uint32_t*>(ws);
-  compact_count_kernel<<<(unsigned)ctas, CP_THREADS, 0, stream>>>(bits, n, counts);
-  compact_write_kernel<<<(unsigned)ctas, CP_THREADS, 0, stream>>>(
-      bits, n, counts, idx, reinterpret_cast<unsigned long long*>(n_acc));
+  const dim3 grid((unsigned)ctas, (unsigned)rows);
+  compact_count_kernel<<<grid, CP_THREADS, 0, stream>>>(bits, n, counts, bstride);
+  compact_write_kernel<<<grid, CP_THREADS, 0, stream>>>(
+      bits, n, counts, idx, reinterpret_cast<unsigned long long*>(n_acc), bstride, istride);
   return 0;
 }
 

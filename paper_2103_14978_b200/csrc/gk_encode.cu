@@ -112,7 +112,6 @@ __global__ void __launch_bounds__(128) encode_tma_kernel(const uint8_t* __restri
     mbar_arrive_expect_tx(&mybar[0], span);
     tma_load_1d(stage, seqs + (4 * b + warp) * (int64_t)span, span, &mybar[0]);
   }
-  uint32_t phase[2] = {0u, 0u};
   for (int i = 0; b < nblocks; ++i, b += gridDim.x) {
     const int buf = i & 1;
     const int64_t bn = b + gridDim.x;
@@ -122,8 +121,7 @@ __global__ void __launch_bounds__(128) encode_tma_kernel(const uint8_t* __restri
       tma_load_1d(stage + (buf ^ 1) * BUF, seqs + (4 * bn + warp) * (int64_t)span, span,
                   &mybar[buf ^ 1]);
     }
-    mbar_wait(&mybar[buf], phase[buf]);
-    phase[buf] ^= 1u;
+    mbar_wait(&mybar[buf], (uint32_t)(i >> 1) & 1u);  // buffer buf's (i>>1)-th use
     const int64_t g = 4 * b + warp;
     uint2* outt = outt0 + (size_t)(i & 1) * 16 * nq;  // double-buffered: one barrier per block
     uint2* myout = outt + (size_t)warp * 4 * nq;

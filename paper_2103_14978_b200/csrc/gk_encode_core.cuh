@@ -230,6 +230,14 @@ __device__ __forceinline__ uint32_t encode_group_v2(const RowAddr<SM4>& ra, int 
       else encode_quad<SM4, LPART, BOFF + 384u>(ra, q, rem, bad, emit);
     }
   }
+  // undefined bases are rare (0.3% of pairs in the paper's Set_3, Table S.1
+  // :509): one warp-wide OR decides whether the per-row flags are needed at all
+  {
+    uint32_t any = 0u;
+#pragma unroll
+    for (int blk = 0; blk < 8; ++blk) any |= bad[blk];
+    if (__reduce_or_sync(0xFFFFFFFFu, any) == 0u) return 0u;
+  }
   uint32_t und = 0u;
 #pragma unroll
   for (int blk = 0; blk < 8; ++blk) {

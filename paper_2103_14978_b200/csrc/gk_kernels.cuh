@@ -23,8 +23,8 @@ int launch_filter_sweep(const uint32_t* reads, const uint32_t* refs, const uint3
 int launch_filter_ascii(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n,
                         int len, int e, uint32_t* accept, uint8_t* errc, cudaStream_t stream);
 
-size_t compact_workspace_bytes(int64_t n);
+size_t compact_workspace_bytes(int64_t n, int rows = 1);
 int launch_compact(const uint32_t* bits, int64_t n, uint32_t* idx, uint64_t* n_acc, void* ws,
-                   cudaStream_t stream);
+                   cudaStream_t stream, int rows = 1, int64_t bstride = 0, int64_t istride = 0);
 
 }  // namespace gk

@@ -78,6 +78,12 @@ def test_argument_validation_before_any_launch(lib):
     assert lib.gk_filter_ascii(P, P, 2000, 10, 100, 2, P, None, None) == -1  # stride limit
     assert lib.gk_compact(P, 10, P, P, P, 0, None) == -5                    # workspace
     assert lib.gk_compact(P, 1 << 33, P, P, P, 1 << 20, None) == -1
+    assert lib.gk_compact_rows(P, 3, 10, 100, P, 100, P, P, 0, None) == -5      # workspace
+    assert lib.gk_compact_rows(P, 3, 2, 100, P, 100, P, P, 1 << 20, None) == -1  # bits stride
+    assert lib.gk_compact_rows(P, 3, 4, 100, P, 50, P, P, 1 << 20, None) == -1   # idx stride
+    assert lib.gk_compact_rows(P, -1, 4, 100, P, 100, P, P, 1 << 20, None) == -1
+    assert lib.gk_compact_rows(P, 0, 4, 100, P, 100, P, P, 0, None) == 0
+    assert lib.gk_compact_rows_workspace_bytes(100_000, 11) >= 11 * 4
     assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 1 << 30, 1000) == -1  # chunk
     assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 10, 1024) == -5
     import ctypes as C

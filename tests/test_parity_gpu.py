@@ -285,6 +285,43 @@ def test_compact_indices(gk, n):
     assert (idx.cpu().numpy()[:expect.size].astype(np.uint32) == expect).all()
 
 
+@pytest.mark.parametrize("n,rows", [(1, 1), (77, 3), (70_001, 11), (300_000, 4)])
+def test_compact_rows(gk, n, rows):
+    rng = np.random.default_rng(n + rows)
+    words = (n + 31) // 32
+    stride = words + 5                                   # padded row stride
+    mat = np.zeros((rows, stride), np.uint32)
+    bits_all = []
+    for r in range(rows):
+        bits = (rng.random(n) < (0.05 + 0.2 * r)).astype(np.uint8)
+        mat[r, :words] = np.packbits(np.concatenate([bits, np.zeros((-n) % 32, np.uint8)]),
+                                     bitorder="little").view(np.uint32)
+        mat[r, words:] = 0xFFFFFFFF                      # padding must be ignored
+        bits_all.append(bits)
+    dw = to_dev(mat.view(np.int32))
+    idx, n_acc = gk.compact_rows(dw, n)
+    torch.cuda.synchronize()
+    for r in range(rows):
+        expect = np.nonzero(bits_all[r])[0]
+        assert int(n_acc[r].item()) == expect.size, r
+        assert (idx[r].cpu().numpy()[:expect.size].astype(np.uint32) == expect).all(), r
+
+
+def test_compact_rows_after_sweep(gk):
+    reads, refs = pairgen.gen_pairs(20_000, 150)
+    dr, df = to_dev(reads), to_dev(refs)
+    q, uq = gk.encode(dr)
+    r, ur = gk.encode(df)
+    acc, _ = gk.filter_sweep(q, r, uq, ur, 20_000, 150, 15)
+    idx, n_acc = gk.compact_rows(acc, 20_000)
+    torch.cuda.synchronize()
+    oa, _ = oracle.sweep(reads, refs, 15)
+    for e in range(16):
+        expect = np.nonzero(oa[e])[0]
+        assert int(n_acc[e].item()) == expect.size
+        assert (idx[e].cpu().numpy()[:expect.size] == expect).all()
+
+
 def test_compact_after_filter(gk):
     reads, refs = pairgen.gen_pairs(20_000, 150)
     dr, df = to_dev(reads), to_dev(refs)
