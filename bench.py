@@ -116,6 +116,24 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def load_traffic(workload):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    kernels of this workload, from the newest committed ncu --set full capture
+    (profiles/r*_traffic.json, written by tools/ncu_traffic.py); None if absent."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json"))):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if d.get("workload") == workload:
+            best = {k.split("(")[0].strip(): int(v["traffic_bytes_per_launch"])
+                    for k, v in d.get("kernels", {}).items()}
+    return best
+
+
 def cpu_baseline(cfg_name, sample_pairs=None, budget_s=15.0):
     """The oracle, as it stands, on this host's cores over a bounded sample."""
     import oracle
@@ -370,22 +388,53 @@ def main():
         alu_ach = n * sweep_ops(es[-1]) / (tot_ms / 1e3) / 1e12
     else:
         alu_ach = sum(n * alg_ops(e) for e in es) / (tot_ms / 1e3) / 1e12
-    if args.path == "fused":
-        roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(hbm_ach / hbm_peak, 4)}
-    elif alu_ach / alu_peak >= hbm_ach / hbm_peak:
-        roof = {"bound": "alu", "achieved": round(alu_ach, 3), "peak": round(alu_peak, 3),
-                "unit": "T int-ops/s", "frac": round(alu_ach / alu_peak, 4)}
+    traffic = load_traffic(f"{args.config}:{args.path}:{n}")
+
+    def entry(kernel, bound, ach, peak, unit, launch_ms, share, extra):
+        d = {"bound": bound, "achieved": round(ach, 3), "peak": round(peak, 3), "unit": unit,
+             "frac": round(ach / peak, 4), "kernel": kernel,
+             "traffic": traffic.get(kernel) if traffic else None,
+             "peak_source": peak_src if unit == "GB/s" else
+             f"derived: 148 SM x 64 ALU lanes/clk x {clk_mhz:.0f} MHz (DESIGN.md section 6)",
+             "mean_launch_ms": round(launch_ms, 4), "share_of_step": round(share, 4)}
+        d.update(extra)
+        return d
+
+    kernels = []
+    fkernel = {"fused": "filter_ascii_tma_kernel", "sweep": "filter_bt_sweep_kernel",
+               "packed": "filter_sp_kernel<E>/filter_bt_kernel"}[args.path]
+    fextra = {"api": kname, "bytes_per_launch": bytes_launch,
+              "ops_per_pair": round(sweep_ops(es[-1]) if args.path == "sweep" else
+                                    sum(alg_ops(e) for e in es) / n_ev, 2),
+              "hbm_frac": round(hbm_ach / hbm_peak, 4), "alu_frac": round(alu_ach / alu_peak, 4)}
+    if args.path == "fused" or hbm_ach / hbm_peak > alu_ach / alu_peak:
+        kernels.append(entry(fkernel, "hbm", hbm_ach, hbm_peak, "GB/s", tot_ms / n_launch,
+                             tot_ms / ms_per_step, fextra))
     else:
-        roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(hbm_ach / hbm_peak, 4)}
-    roof.update({"kernel": kname, "traffic": None, "peak_source": peak_src,
-                 "alu_peak_basis": f"148 SM x 64 ALU lanes/clk x {clk_mhz:.0f} MHz (B200_PROFILING.md / B300_MICROARCH.md)",
-                 "hbm_frac": round(hbm_ach / hbm_peak, 4), "alu_frac": round(alu_ach / alu_peak, 4),
-                 "bytes_per_launch": bytes_launch, "mean_launch_ms": round(tot_ms / n_launch, 4),
-                 "ops_per_pair": round(sweep_ops(es[-1]) if args.path == "sweep" else
-                                       sum(alg_ops(e) for e in es) / n_ev, 2),
-                 "share_of_step": round(tot_ms / ms_per_step, 4)})
+        kernels.append(entry(fkernel, "alu", alu_ach, alu_peak, "T int-ops/s", tot_ms / n_launch,
+                             tot_ms / ms_per_step, fextra))
+    if args.path in ("packed", "sweep"):
+        enc_bytes_launch = n * L + n * L / 4 + n / 8
+        kernels.append(entry("encode_tma_kernel<128, 0, 0>" if L <= 128 else "encode_tma_kernel",
+                             "hbm", enc_bytes_launch / (enc_ms / 2 / 1e3) / 1e9, hbm_peak, "GB/s",
+                             enc_ms / 2, enc_ms / ms_per_step,
+                             {"api": "gk_encode (2 launches per step: reads, reference segments)",
+                              "bytes_per_launch": enc_bytes_launch}))
+    comp_tot = sum(comp_ms[:n_rec])
+    if comp_tot > 0:
+        n_claunch = 1 if args.path == "sweep" else n_ev
+        comp_bytes = (2 * (n / 8) + 4 * sum(int(x) for x in n_acc_tot) / world) / n_claunch
+        kernels.append(entry("compact_write_kernel", "hbm",
+                             comp_bytes / (comp_tot / n_claunch / 1e3) / 1e9, hbm_peak, "GB/s",
+                             comp_tot / n_claunch, comp_tot / ms_per_step,
+                             {"api": "gk_compact_rows (all e)" if args.path == "sweep"
+                              else "gk_compact per e", "bytes_per_launch": comp_bytes,
+                              "note": "count + write kernels; bytes = accept bits read twice + indices"}))
+    # the dominant kernel = the largest share of the step
+    roof = dict(max(kernels, key=lambda k: k["share_of_step"]))
+    roof["all_kernels"] = [{k: v for k, v in x.items() if k in ("kernel", "bound", "frac", "achieved",
+                                                               "unit", "share_of_step", "traffic")}
+                           for x in kernels]
     per_e = {}
     for j, e in enumerate(es):
         if args.path == "sweep":
