@@ -333,6 +333,27 @@ def main():
     if world > 1:
         dist.barrier()
 
+    # accuracy (outside the timed region): the paper's FA / FR study (Tables S.2-S.6)
+    # on the whole batch -- exact edit distance on the device (gk_edit_distance)
+    # against the sweep's decisions (gk_accuracy)
+    accuracy = None
+    if args.path == "sweep":
+        v0 = torch.cuda.Event(enable_timing=True)
+        v1 = torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        dist = gk.edit_distance(reads, refs, L, stream=stream)
+        v1.record(stream)
+        counts = gk.accuracy(accept, errc, dist, n, es, stream=stream)
+        torch.cuda.synchronize(dev)
+        counts = sharding.sum_over_ranks(counts.flatten(), device=dev)
+        accuracy = {"verifier": "gk_edit_distance (Myers bit-vector, exact global distance)",
+                    "verifier_ms": round(v0.elapsed_time(v1), 3),
+                    "per_e": {str(e): {"accept_rate": round(counts[4 * j + 1] / max(1, counts[4 * j]), 5),
+                                       "false_accept_rate": round(counts[4 * j + 2] / max(1, counts[4 * j]), 5),
+                                       "false_rejects": int(counts[4 * j + 3])}
+                              for j, e in enumerate(es)}}
+        del dist
+
     # the per-e packed path on the same data (context for the sweep's speed-up)
     alt = None
     if args.path == "sweep" and not args.no_alt:
@@ -485,6 +506,7 @@ def main():
             "encode": encode,
             "per_e": per_e,
             "alt_path": alt,
+            "accuracy": accuracy,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "e2e": e2e,

@@ -175,6 +175,30 @@ int gk_compact_rows(const uint32_t* d_accept_bits, int32_t n_rows, int64_t bits_
                     int64_t n_pairs, uint32_t* d_idx, int64_t idx_row_stride, uint64_t* d_n_acc,
                     void* d_ws, size_t ws_bytes, void* stream);
 
+/* Accuracy harness: the ground truth of the paper's
+ * accuracy study -- exact global edit distance, as Edlib in global mode
+ * -- and the false-accept / false-reject tallies of filter
+ * decisions (Tables S.2-S.12).  Not on the filtering path.
+ *
+ * gk_edit_distance: Levenshtein distance of the first len bytes of read p and
+ * reference segment p (rows of `stride` bytes, as gk_filter_ascii), bytes
+ * compared exactly; Myers' bit-vector algorithm, one thread per pair.
+ *  d_dist : n_pairs int32 (written).
+ * Errors: GK_ERR_ARG, GK_ERR_LEN, GK_ERR_ALIGN, GK_ERR_CUDA. */
+int gk_edit_distance(const uint8_t* d_reads, const uint8_t* d_refs, int64_t stride,
+                     int64_t n_pairs, int32_t len, int32_t* d_dist, void* stream);
+
+/* gk_accuracy: for each row r of decisions (threshold d_e_list[r], accept bits
+ * at d_accept_bits + r*bits_row_stride, error counts at d_errcount +
+ * r*err_row_stride), d_counts[4r .. 4r+3] = {defined pairs, accepted, false
+ * accepts (accepted, dist > e), false rejects (rejected, dist <= e)}; pairs
+ * with error count 255 (undefined) are left out.
+ *  d_e_list : n_rows int32 in device memory.  d_counts : 4*n_rows u64 (written).
+ * Errors: GK_ERR_ARG, GK_ERR_ALIGN, GK_ERR_CUDA. */
+int gk_accuracy(const uint32_t* d_accept_bits, int64_t bits_row_stride, const uint8_t* d_errcount,
+                int64_t err_row_stride, const int32_t* d_dist, int64_t n_pairs,
+                const int32_t* d_e_list, int32_t n_rows, uint64_t* d_counts, void* stream);
+
 /* End-to-end from HOST buffers (the paper's "filter time"): streams
  * the pairs through device memory in chunks, overlapping host->device copies,
  * filtering and device->host copies on two CUDA streams.

@@ -58,6 +58,8 @@ def load_library(path: str = LIB_PATH):
         "gk_compact_workspace_bytes": (SZ, [I64]),
         "gk_compact": (ctypes.c_int, [P, I64, P, P, P, SZ, P]),
         "gk_compact_rows_workspace_bytes": (SZ, [I64, I32]),
+        "gk_edit_distance": (ctypes.c_int, [P, P, I64, I64, I32, P, P]),
+        "gk_accuracy": (ctypes.c_int, [P, I64, P, I64, P, I64, P, I32, P, P]),
         "gk_compact_rows": (ctypes.c_int, [P, I32, I64, I64, P, I64, P, P, SZ, P]),
         "gk_host_workspace_bytes": (SZ, [I64, I64]),
         "gk_filter_host": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P, SZ, I64]),
@@ -218,6 +220,33 @@ def compact_rows(accept, n: int, idx=None, n_acc=None, workspace=None, want_indi
                                           workspace.data_ptr(), workspace.numel(),
                                           _stream(stream)), "gk_compact_rows")
     return idx, n_acc
+
+
+# ---- accuracy harness (not on the filtering path) ------------------------------
+def edit_distance(reads, refs, length: int | None = None, out=None, stream=None):
+    """Exact global edit distance of every (read, ref) row pair -> int32 [n]."""
+    import torch
+    n, stride = reads.shape
+    length = stride if length is None else length
+    if out is None:
+        out = torch.empty(max(1, n), dtype=torch.int32, device=reads.device)
+    _check(load_library().gk_edit_distance(reads.data_ptr(), refs.data_ptr(), stride, n, length,
+                                           out.data_ptr(), _stream(stream)), "gk_edit_distance")
+    return out
+
+
+def accuracy(accept, errcount, dist, n: int, e_list, stream=None):
+    """False-accept / false-reject tallies of decision rows (accept [rows, words],
+    errcount [rows, n]) against distances -> int64 [rows, 4] (defined, accepted,
+    false accepts, false rejects)."""
+    import torch
+    rows = accept.shape[0]
+    es = torch.tensor(list(e_list), dtype=torch.int32, device=accept.device)
+    counts = torch.empty((rows, 4), dtype=torch.int64, device=accept.device)
+    _check(load_library().gk_accuracy(accept.data_ptr(), accept.stride(0), errcount.data_ptr(),
+                                      errcount.stride(0), dist.data_ptr(), n, es.data_ptr(), rows,
+                                      counts.data_ptr(), _stream(stream)), "gk_accuracy")
+    return counts
 
 
 # ---- end to end from host buffers ----------------------------------------------

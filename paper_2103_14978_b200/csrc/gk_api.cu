@@ -6,6 +6,14 @@
 #include "../../include/gatekeeper.h"
 #include "gk_kernels.cuh"
 
+namespace gk {
+int launch_edit_distance(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n,
+                         int len, int32_t* dist, cudaStream_t stream);
+int launch_accuracy(const uint32_t* accept, int64_t astride, const uint8_t* errc, int64_t estride,
+                    const int32_t* dist, int64_t n, const int32_t* e_list, int rows,
+                    unsigned long long* counts, cudaStream_t stream);
+}  // namespace gk
+
 static thread_local int g_last_cuda_error = 0;
 
 static int cuda_status(cudaError_t err) {
@@ -172,6 +180,37 @@ int gk_compact_rows(const uint32_t* d_accept_bits, int32_t n_rows, int64_t bits_
   if (!d_ws || ws_bytes < gk::compact_workspace_bytes(n_pairs, n_rows)) return GK_ERR_WORKSPACE;
   gk::launch_compact(d_accept_bits, n_pairs, d_idx, d_n_acc, d_ws, (cudaStream_t)stream, n_rows,
                      bits_row_stride, idx_row_stride);
+  return after_launch();
+}
+
+int gk_edit_distance(const uint8_t* d_reads, const uint8_t* d_refs, int64_t stride,
+                     int64_t n_pairs, int32_t len, int32_t* d_dist, void* stream) {
+  int rc = check_ascii(d_reads, n_pairs, len, stride);
+  if (rc) return rc;
+  if (n_pairs == 0) return GK_OK;
+  if (!d_refs || !d_dist) return GK_ERR_ARG;
+  if (!aligned(d_dist, 4)) return GK_ERR_ALIGN;
+  gk::launch_edit_distance(d_reads, d_refs, stride, n_pairs, len, d_dist, (cudaStream_t)stream);
+  return after_launch();
+}
+
+int gk_accuracy(const uint32_t* d_accept_bits, int64_t bits_row_stride, const uint8_t* d_errcount,
+                int64_t err_row_stride, const int32_t* d_dist, int64_t n_pairs,
+                const int32_t* d_e_list, int32_t n_rows, uint64_t* d_counts, void* stream) {
+  if (n_pairs < 0 || n_rows < 0 || n_rows > 65535) return GK_ERR_ARG;
+  if (n_rows == 0) return GK_OK;
+  if (!d_counts || !d_e_list) return GK_ERR_ARG;
+  if (!aligned(d_counts, 8) || !aligned(d_e_list, 4)) return GK_ERR_ALIGN;
+  if (n_pairs == 0)
+    return cuda_status(cudaMemsetAsync(d_counts, 0, 32 * (size_t)n_rows, (cudaStream_t)stream));
+  if (!d_accept_bits || !d_errcount || !d_dist) return GK_ERR_ARG;
+  if (n_rows > 1 && (bits_row_stride < (int64_t)gk_result_words(n_pairs) ||
+                     err_row_stride < n_pairs))
+    return GK_ERR_ARG;
+  if (!aligned(d_accept_bits, 4) || !aligned(d_dist, 4)) return GK_ERR_ALIGN;
+  gk::launch_accuracy(d_accept_bits, bits_row_stride, d_errcount, err_row_stride, d_dist, n_pairs,
+                      d_e_list, n_rows, reinterpret_cast<unsigned long long*>(d_counts),
+                      (cudaStream_t)stream);
   return after_launch();
 }
 

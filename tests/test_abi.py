@@ -84,6 +84,14 @@ def test_argument_validation_before_any_launch(lib):
     assert lib.gk_compact_rows(P, -1, 4, 100, P, 100, P, P, 1 << 20, None) == -1
     assert lib.gk_compact_rows(P, 0, 4, 100, P, 100, P, P, 0, None) == 0
     assert lib.gk_compact_rows_workspace_bytes(100_000, 11) >= 11 * 4
+    assert lib.gk_edit_distance(P, P, 100, 10, 0, P, None) == -2
+    assert lib.gk_edit_distance(P, P, 99, 10, 100, P, None) == -1
+    assert lib.gk_edit_distance(P, None, 100, 10, 100, P, None) == -1
+    assert lib.gk_edit_distance(P, P, 100, 10, 100, P + 2, None) == -4
+    assert lib.gk_edit_distance(None, None, 100, 0, 100, None, None) == 0
+    assert lib.gk_accuracy(P, 4, P, 100, P, 100, P, 2, None, None) == -1    # no counts
+    assert lib.gk_accuracy(P, 1, P, 100, P, 100, P, 2, P, None) == -1       # bits stride
+    assert lib.gk_accuracy(P, 4, P, 100, P, 100, P, 0, P, None) == 0
     assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 1 << 30, 1000) == -1  # chunk
     assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 10, 1024) == -5
     import ctypes as C

@@ -270,6 +270,58 @@ def test_sweep_kernel_full_size_sampled(gk):
             assert (bits == oa[e]).all() and (err[e, s:s + 4096].cpu().numpy() == oc[e]).all(), (s, e)
 
 
+# ---------------------------------------------------------------- verifier -----
+@pytest.mark.parametrize("L", [1, 2, 7, 31, 63, 64, 65, 100, 127, 128, 129, 150, 250, 300, 508])
+def test_edit_distance_matches_textbook_dp(gk, L):
+    """gk_edit_distance (Myers bit-vector) == the oracle's textbook Levenshtein DP."""
+    n = 3000 if L <= 150 else 800
+    reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED,
+                                    emax=max(1, L // 5), seed=L + 555)
+    d = gk.edit_distance(to_dev(reads), to_dev(refs))
+    torch.cuda.synchronize()
+    od = oracle.edit_distance(reads, refs)
+    bad = np.nonzero(d.cpu().numpy()[:n] != od)[0]
+    assert bad.size == 0, (L, bad[:5], d.cpu().numpy()[bad[:5]], od[bad[:5]])
+
+
+def test_edit_distance_odd_bytes_and_strides(gk):
+    L, n, stride = 90, 1500, 97
+    reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, emax=9, stride=stride,
+                                    seed=77)
+    rng = np.random.default_rng(3)
+    rows = rng.choice(n, 200, replace=False)
+    reads[rows, rng.integers(0, L, 200)] = ord("N")
+    refs[rows[:100], rng.integers(0, L, 100)] = ord("N")
+    refs[rows[100:], rng.integers(0, L, 100)] = rng.integers(0, 256, 100).astype(np.uint8)
+    reads[:50] = np.where(reads[:50] < 0x80, reads[:50] | 0x20, reads[:50])   # lower case
+    d = gk.edit_distance(to_dev(reads), to_dev(refs), L)
+    torch.cuda.synchronize()
+    od = oracle.edit_distance(reads, refs, L)
+    assert (d.cpu().numpy()[:n] == od).all()
+
+
+def test_accuracy_tallies(gk):
+    """gk_accuracy over the sweep rows == numpy tallies of the oracle's decisions
+    against the oracle's distances (the paper's FA / FR definitions, :224, :530)."""
+    n, L, emax = 20_000, 100, 10
+    reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, emax=emax, seed=9)
+    dr, df = to_dev(reads), to_dev(refs)
+    q, uq = gk.encode(dr)
+    r, ur = gk.encode(df)
+    acc, err = gk.filter_sweep(q, r, uq, ur, n, L, emax)
+    dist = gk.edit_distance(dr, df)
+    counts = gk.accuracy(acc, err, dist, n, range(emax + 1)).cpu().numpy()
+    oa, oc = oracle.sweep(reads, refs, emax)
+    od = oracle.edit_distance(reads, refs)
+    for e in range(emax + 1):
+        defined = oc[e] != 255
+        expect = [defined.sum(), (oa[e].astype(bool) & defined).sum(),
+                  (oa[e].astype(bool) & defined & (od > e)).sum(),
+                  (~oa[e].astype(bool) & defined & (od <= e)).sum()]
+        assert list(counts[e]) == [int(x) for x in expect], (e, counts[e], expect)
+        assert counts[e][3] == 0          # no false rejects (the paper's claim)
+
+
 # ---------------------------------------------------------------- compact ------
 @pytest.mark.parametrize("n", [1, 77, 4096, 70_001, 300_000])
 def test_compact_indices(gk, n):

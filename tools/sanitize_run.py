@@ -1,7 +1,8 @@
 """Small invocation of every kernel of libgk.so, for compute-sanitizer runs
 (memcheck / racecheck / synccheck / initcheck): TMA encoder + tail paths, the
 register filter, the block-transposed filter and its e sweep, the mask-major fallback, the fused
-ASCII filter, compaction and the host pipelines."""
+ASCII filter, compaction (single and batched), the accuracy harness and the host
+pipelines."""
 import os
 import sys
 
@@ -25,6 +26,10 @@ for L, n in [(100, 3000), (150, 2200), (37, 1500)]:
         gk.filter_sweep(q, s, uq, us, n, L, e)
         gk.filter_ascii(r, f, e, L)
         gk.compact(acc, n)
+    d = gk.edit_distance(r, f, L)
+    a2, e2 = gk.filter_sweep(q, s, uq, us, n, L, 4)
+    gk.accuracy(a2, e2, d, n, range(5))
+    gk.compact_rows(a2, n)
     torch.cuda.synchronize()
     acc, _ = gk.filter_host(torch.from_numpy(hr).pin_memory(), torch.from_numpy(hf).pin_memory(),
                             4, chunk_pairs=1024)
