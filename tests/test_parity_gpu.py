@@ -270,6 +270,80 @@ def test_sweep_kernel_full_size_sampled(gk):
             assert (bits == oa[e]).all() and (err[e, s:s + 4096].cpu().numpy() == oc[e]).all(), (s, e)
 
 
+# ---------------------------------------------------------------- index mode ---
+def make_index_case(G, n_reads, n_cand, L, seed):
+    """A synthetic genome (uniform bases, a few 'N' runs, some lower case), reads
+    drawn from it with edits, and candidate (read, position) pairs: half at the
+    read's true position (or near it), half random."""
+    rng = np.random.default_rng(seed)
+    genome = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, G)].copy()
+    for s0 in rng.integers(0, G - 50, 6):
+        genome[s0:s0 + rng.integers(1, 40)] = ord("N")
+    low = rng.integers(0, G - 5000)
+    genome[low:low + 3000] |= 0x20
+    true_pos = rng.integers(0, G - L - 8, n_reads)
+    reads = np.empty((n_reads, L), np.uint8)
+    for r in range(n_reads):
+        seg = genome[true_pos[r]:true_pos[r] + L + 8].copy()
+        for _ in range(rng.integers(0, 6)):
+            kind, i = rng.integers(0, 3), rng.integers(0, L)
+            if kind == 0:
+                seg[i] = b"ACGT"[rng.integers(0, 4)]
+            elif kind == 1:
+                seg = np.delete(seg, i)
+            else:
+                seg = np.insert(seg, i, b"ACGT"[rng.integers(0, 4)])
+        reads[r] = seg[:L]
+    read_id = rng.integers(0, n_reads, n_cand)
+    pos = np.where(rng.random(n_cand) < 0.5,
+                   np.clip(true_pos[read_id] + rng.integers(-3, 4, n_cand), 0, G - L),
+                   rng.integers(0, G - L + 1, n_cand))
+    return genome, reads, read_id.astype(np.int64), pos.astype(np.int64)
+
+
+@pytest.mark.parametrize("L,emax", [(100, 10), (150, 15), (37, 6), (250, 25)])
+def test_reference_index_mode(gk, L, emax):
+    """pack_planes + gather_windows + filter_sweep == the oracle on the ASCII
+    windows the candidates name (section 3.5)."""
+    G, n_reads, n_cand = 200_003, 3000, 9000
+    genome, reads, read_id, pos = make_index_case(G, n_reads, n_cand, L, seed=L)
+    gp = gk.pack_planes(to_dev(genome.reshape(1, -1)))
+    rp = gk.pack_planes(to_dev(reads))
+    q, uq = gk.gather_windows(rp, n_reads * L, to_dev(read_id * L), L)
+    r, ur = gk.gather_windows(gp, G, to_dev(pos), L)
+    acc, err = gk.filter_sweep(q, r, uq, ur, n_cand, L, emax)
+    torch.cuda.synchronize()
+    ref_rows = np.stack([genome[p:p + L] for p in pos])
+    read_rows = reads[read_id]
+    # the gathered packed words equal gk_encode of the ASCII windows
+    q2, uq2 = gk.encode(to_dev(read_rows))
+    r2, ur2 = gk.encode(to_dev(ref_rows))
+    torch.cuda.synchronize()
+    assert torch.equal(uq, uq2) and torch.equal(ur, ur2)
+    oa, oc = oracle.sweep(read_rows, ref_rows, emax)
+    for e in range(emax + 1):
+        a = unpack_accept(acc[e], n_cand)
+        c = err[e].cpu().numpy()[:n_cand]
+        bad = np.nonzero((a != oa[e]) | (c != oc[e]))[0]
+        assert bad.size == 0, (L, e, bad[:5])
+
+
+def test_reference_index_out_of_range_windows(gk):
+    L, G = 50, 10_000
+    genome, reads, read_id, pos = make_index_case(G, 100, 2100, L, seed=5)
+    pos[::7] = G - L + 3        # runs past the end
+    pos[1::7] = -2              # before the start
+    gp = gk.pack_planes(to_dev(genome.reshape(1, -1)))
+    rp = gk.pack_planes(to_dev(reads))
+    q, uq = gk.gather_windows(rp, 100 * L, to_dev(read_id * L), L)
+    r, ur = gk.gather_windows(gp, G, to_dev(pos), L)
+    acc, err = gk.filter(q, r, uq, ur, 2100, L, 3)
+    torch.cuda.synchronize()
+    e = err.cpu().numpy()[:2100]
+    assert (e[::7] == 255).all() and (e[1::7] == 255).all()
+    assert (unpack_accept(acc, 2100)[::7] == 1).all()
+
+
 # ---------------------------------------------------------------- verifier -----
 @pytest.mark.parametrize("L", [1, 2, 7, 31, 63, 64, 65, 100, 127, 128, 129, 150, 250, 300, 508])
 def test_edit_distance_matches_textbook_dp(gk, L):
