@@ -181,18 +181,20 @@ int gk_compact_rows(const uint32_t* d_accept_bits, int32_t n_rows, int64_t bits_
  * neither an ASCII copy of every reference segment nor a per-pair encode is
  * needed.  Reads are packed the same way (row r = bases [r*len, r*len+len)).
  *
- * Bit planes of n_bases bases: three u32 arrays of gk_plane_words(n_bases)
- * words; bit b of word w describes base 32w+b: hi = high code bit, lo = low
- * code bit (A=00 C=01 G=10 T=11), undef = 1 iff the byte is not
- * one of A C G T a c g t (:95, reading R8; its code bits are 0).  One word of
- * look-ahead past the last base is included (and zeroed). */
+ * Bit planes of n_bases bases: gk_plane_words(n_bases) blocks of 4 u32
+ * (16 bytes, interleaved so that a window at a random offset touches 2-3
+ * sectors): block w = {hi, lo, undef, 0}, bit b of each describing base
+ * 32w+b: hi = high code bit, lo = low code bit (A=00 C=01 G=10 T=11,
+ * PAPER.md:49), undef = 1 iff the byte is not one of A C G T a c g t (:95,
+ * reading R8; its code bits are 0).  One block of look-ahead past the last
+ * base is included (and zeroed).  The array must be 16-byte aligned. */
 size_t gk_plane_words(int64_t n_bases);
 
 /* ASCII rows -> bit planes: base i of row r (byte d_rows[r*stride + i], i < len)
  * is base r*len + i of the planes (n_bases = n_rows*len; a genome is one row).
  * Errors: GK_ERR_ARG, GK_ERR_LEN, GK_ERR_ALIGN, GK_ERR_CUDA. */
 int gk_pack_planes(const uint8_t* d_rows, int64_t n_rows, int32_t len, int64_t stride,
-                   uint32_t* d_hi, uint32_t* d_lo, uint32_t* d_undef_plane, void* stream);
+                   uint32_t* d_planes, void* stream);
 
 /* Windows -> the packed layout gk_filter / gk_filter_sweep consume: sequence p
  * of the output (n_pairs sequences of `len` bases, gk_packed_words(n_pairs, len)
@@ -202,9 +204,9 @@ int gk_pack_planes(const uint8_t* d_rows, int64_t n_rows, int32_t len, int64_t s
  * flagged undefined (the pair is accepted with error count 255).
  *  d_offsets : n_pairs int64 base offsets in device memory (8-byte aligned).
  * Errors: GK_ERR_ARG, GK_ERR_LEN, GK_ERR_ALIGN, GK_ERR_CUDA. */
-int gk_gather_windows(const uint32_t* d_hi, const uint32_t* d_lo, const uint32_t* d_undef_plane,
-                      int64_t n_bases, const int64_t* d_offsets, int64_t n_pairs, int32_t len,
-                      uint32_t* d_packed, uint32_t* d_undef, void* stream);
+int gk_gather_windows(const uint32_t* d_planes, int64_t n_bases, const int64_t* d_offsets,
+                      int64_t n_pairs, int32_t len, uint32_t* d_packed, uint32_t* d_undef,
+                      void* stream);
 
 /* Accuracy harness: the ground truth of the paper's
  * accuracy study -- exact global edit distance, as Edlib in global mode

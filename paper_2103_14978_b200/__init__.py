@@ -60,8 +60,8 @@ def load_library(path: str = LIB_PATH):
         "gk_compact_rows_workspace_bytes": (SZ, [I64, I32]),
         "gk_edit_distance": (ctypes.c_int, [P, P, I64, I64, I32, P, P]),
         "gk_plane_words": (SZ, [I64]),
-        "gk_pack_planes": (ctypes.c_int, [P, I64, I32, I64, P, P, P, P]),
-        "gk_gather_windows": (ctypes.c_int, [P, P, P, I64, P, I64, I32, P, P, P]),
+        "gk_pack_planes": (ctypes.c_int, [P, I64, I32, I64, P, P]),
+        "gk_gather_windows": (ctypes.c_int, [P, I64, P, I64, I32, P, P, P]),
         "gk_accuracy": (ctypes.c_int, [P, I64, P, I64, P, I64, P, I32, P, P]),
         "gk_compact_rows": (ctypes.c_int, [P, I32, I64, I64, P, I64, P, P, SZ, P]),
         "gk_host_workspace_bytes": (SZ, [I64, I64]),
@@ -227,17 +227,16 @@ def compact_rows(accept, n: int, idx=None, n_acc=None, workspace=None, want_indi
 
 # ---- reference-index mode -----------------------------------------------------
 def pack_planes(rows, length: int | None = None, stream=None):
-    """ASCII rows (uint8 CUDA [n_rows, stride]; a genome is one row) -> bit planes
-    (hi, lo, undef) as int32 tensors of gk_plane_words(n_rows*length) words."""
+    """ASCII rows (uint8 CUDA [n_rows, stride]; a genome is one row) -> interleaved bit
+    planes, int32 [gk_plane_words(n_rows*length), 4] = (hi, lo, undef, 0) per 32 bases."""
     import torch
     n_rows, stride = rows.shape
     length = stride if length is None else length
     words = load_library().gk_plane_words(n_rows * length)
-    planes = [torch.empty(words, dtype=torch.int32, device=rows.device) for _ in range(3)]
+    planes = torch.empty((words, 4), dtype=torch.int32, device=rows.device)
     _check(load_library().gk_pack_planes(rows.data_ptr(), n_rows, length, stride,
-                                         *(t.data_ptr() for t in planes), _stream(stream)),
-           "gk_pack_planes")
-    return tuple(planes)
+                                         planes.data_ptr(), _stream(stream)), "gk_pack_planes")
+    return planes
 
 
 def gather_windows(planes, n_bases: int, offsets, length: int, out=None, stream=None):
@@ -251,10 +250,9 @@ def gather_windows(planes, n_bases: int, offsets, length: int, out=None, stream=
         undef = torch.empty(max(1, undef_words(n)), dtype=torch.int32, device=dev)
     else:
         packed, undef = out
-    hi, lo, bad = planes
-    _check(load_library().gk_gather_windows(hi.data_ptr(), lo.data_ptr(), bad.data_ptr(), n_bases,
-                                            offsets.data_ptr(), n, length, packed.data_ptr(),
-                                            undef.data_ptr(), _stream(stream)),
+    _check(load_library().gk_gather_windows(planes.data_ptr(), n_bases, offsets.data_ptr(), n,
+                                            length, packed.data_ptr(), undef.data_ptr(),
+                                            _stream(stream)),
            "gk_gather_windows")
     return packed, undef
 

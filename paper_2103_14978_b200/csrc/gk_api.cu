@@ -12,11 +12,10 @@ int launch_edit_distance(const uint8_t* reads, const uint8_t* refs, int64_t stri
 int launch_accuracy(const uint32_t* accept, int64_t astride, const uint8_t* errc, int64_t estride,
                     const int32_t* dist, int64_t n, const int32_t* e_list, int rows,
                     unsigned long long* counts, cudaStream_t stream);
-int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int len, int64_t stride, uint32_t* hi,
-                       uint32_t* lo, uint32_t* bad, cudaStream_t stream);
-int launch_gather_windows(const uint32_t* hi, const uint32_t* lo, const uint32_t* bad,
-                          int64_t nbases, const int64_t* offsets, int64_t n, int len,
-                          uint32_t* packed, uint32_t* undef, cudaStream_t stream);
+int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int len, int64_t stride,
+                       uint32_t* planes, cudaStream_t stream);
+int launch_gather_windows(const uint32_t* planes, int64_t nbases, const int64_t* offsets, int64_t n,
+                          int len, uint32_t* packed, uint32_t* undef, cudaStream_t stream);
 }  // namespace gk
 
 static thread_local int g_last_cuda_error = 0;
@@ -194,29 +193,28 @@ size_t gk_plane_words(int64_t n_bases) {
 }
 
 int gk_pack_planes(const uint8_t* d_rows, int64_t n_rows, int32_t len, int64_t stride,
-                   uint32_t* d_hi, uint32_t* d_lo, uint32_t* d_undef_plane, void* stream) {
+                   uint32_t* d_planes, void* stream) {
   if (n_rows < 0 || stride < len) return GK_ERR_ARG;
   if (len < 1) return GK_ERR_LEN;
   if (n_rows == 0) return GK_OK;
-  if (!d_rows || !d_hi || !d_lo || !d_undef_plane) return GK_ERR_ARG;
-  if (!aligned(d_hi, 4) || !aligned(d_lo, 4) || !aligned(d_undef_plane, 4)) return GK_ERR_ALIGN;
-  gk::launch_pack_planes(d_rows, n_rows, len, stride, d_hi, d_lo, d_undef_plane,
-                         (cudaStream_t)stream);
+  if (!d_rows || !d_planes) return GK_ERR_ARG;
+  if (!aligned(d_planes, 16)) return GK_ERR_ALIGN;
+  gk::launch_pack_planes(d_rows, n_rows, len, stride, d_planes, (cudaStream_t)stream);
   return after_launch();
 }
 
-int gk_gather_windows(const uint32_t* d_hi, const uint32_t* d_lo, const uint32_t* d_undef_plane,
-                      int64_t n_bases, const int64_t* d_offsets, int64_t n_pairs, int32_t len,
-                      uint32_t* d_packed, uint32_t* d_undef, void* stream) {
+int gk_gather_windows(const uint32_t* d_planes, int64_t n_bases, const int64_t* d_offsets,
+                      int64_t n_pairs, int32_t len, uint32_t* d_packed, uint32_t* d_undef,
+                      void* stream) {
   if (n_pairs < 0 || n_bases < 0) return GK_ERR_ARG;
   if (len < 1 || len > GK_MAX_LEN) return GK_ERR_LEN;
   if (n_pairs == 0) return GK_OK;
-  if (!d_hi || !d_lo || !d_undef_plane || !d_offsets || !d_packed || !d_undef) return GK_ERR_ARG;
+  if (!d_planes || !d_offsets || !d_packed || !d_undef) return GK_ERR_ARG;
   if (!aligned(d_packed, 16) || !aligned(d_undef, 4) || !aligned(d_offsets, 8) ||
-      !aligned(d_hi, 4) || !aligned(d_lo, 4) || !aligned(d_undef_plane, 4))
+      !aligned(d_planes, 16))
     return GK_ERR_ALIGN;
-  gk::launch_gather_windows(d_hi, d_lo, d_undef_plane, n_bases, d_offsets, n_pairs, len, d_packed,
-                            d_undef, (cudaStream_t)stream);
+  gk::launch_gather_windows(d_planes, n_bases, d_offsets, n_pairs, len, d_packed, d_undef,
+                            (cudaStream_t)stream);
   return after_launch();
 }
 

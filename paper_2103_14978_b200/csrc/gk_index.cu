@@ -8,7 +8,7 @@
 // the same way (row r at bits [r*L, r*L+L)), so a read with many candidates is
 // encoded once.
 //
-// gather: one warp per group of 32 pairs (lane j = pair j).  For each chunk of
+// gather: one CTA per tile, one warp per group of 32 pairs (lane j = pair j).  For each chunk of
 // 32 positions lane j funnel-shifts its window bits out of two plane words
 // (any bit offset), then a 5-stage shuffle transpose of the 32x32 bit matrix
 // turns "32 positions of pair j" into "position i of 32 pairs" -- the
@@ -23,9 +23,7 @@ namespace gk {
 // bit r*len + i.  Code: high = ASCII bit 2, low = bit 1 ^ bit 2 (as gk_encode);
 // undefined = not one of A C G T a c g t.
 __global__ void pack_planes_kernel(const uint8_t* __restrict__ rows, int64_t n_rows, int len,
-                                   int64_t stride, uint32_t* __restrict__ hi,
-                                   uint32_t* __restrict__ lo, uint32_t* __restrict__ bad,
-                                   int64_t nwords) {
+                                   int64_t stride, uint4* __restrict__ planes, int64_t nwords) {
   const int64_t total = n_rows * (int64_t)len;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
        w += (int64_t)gridDim.x * blockDim.x) {
@@ -46,9 +44,7 @@ __global__ void pack_planes_kernel(const uint8_t* __restrict__ rows, int64_t n_r
         ++r;
       }
     }
-    hi[w] = h;
-    lo[w] = l;
-    bad[w] = b;
+    planes[w] = make_uint4(h, l, b, 0u);
   }
 }
 
@@ -70,65 +66,79 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
   return x;
 }
 
-__device__ __forceinline__ uint32_t plane_bits(const uint32_t* __restrict__ p, int64_t bit) {
+// Bits [bit, bit+32) of the three planes: two 16-byte loads (the planes of a
+// 32-base block are interleaved, so a random window touches 2-3 sectors, not 6).
+__device__ __forceinline__ void window_bits(const uint4* __restrict__ p, int64_t bit, uint32_t& h,
+                                            uint32_t& l, uint32_t& b) {
   const int64_t w = bit >> 5;
   const uint32_t sh = (uint32_t)(bit & 31);
-  return __funnelshift_r(__ldg(p + w), __ldg(p + w + 1), sh);
+  const uint4 a = __ldg(p + w), c = __ldg(p + w + 1);
+  h = __funnelshift_r(a.x, c.x, sh);
+  l = __funnelshift_r(a.y, c.y, sh);
+  b = __funnelshift_r(a.z, c.z, sh);
 }
 
-__global__ void __launch_bounds__(128) gather_windows_kernel(
-    const uint32_t* __restrict__ hi, const uint32_t* __restrict__ lo,
-    const uint32_t* __restrict__ bad, int64_t nbases, const int64_t* __restrict__ offsets,
-    int64_t n, int len, uint32_t* __restrict__ packed, uint32_t* __restrict__ undef,
-    int64_t ngroups_total) {
+// One CTA of 32 warps per tile of 1024 pairs (warp = group of 32 pairs, lane =
+// pair).  Per chunk of 32 positions each warp transposes its words into a
+// shared [32 positions][32 groups] staging tile, so the tile's chunk -- 32 x
+// 256 contiguous bytes of the packed layout -- leaves in full, coalesced lines
+// (a warp alone would write 8-byte pieces at a 256-byte stride).
+__global__ void __launch_bounds__(1024) gather_windows_kernel(
+    const uint4* __restrict__ planes, int64_t nbases, const int64_t* __restrict__ offsets,
+    int64_t n, int len, uint32_t* __restrict__ packed, uint32_t* __restrict__ undef) {
+  __shared__ uint2 stage[32][32];  // [position in chunk][group in tile]
   const int lane = threadIdx.x & 31;
-  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (g >= ngroups_total) return;
+  const int warp = threadIdx.x >> 5;
+  const int64_t tile = blockIdx.x;
+  const int64_t g = tile * 32 + warp;
   const int64_t p = g * 32 + lane;
-  const int64_t tile = g >> 5;
-  const int gl = (int)(g & 31);
   int64_t off = p < n ? offsets[p] : -1;
   // a window outside [0, nbases) makes the pair undefined (accepted, 255)
-  bool oob = p < n && (off < 0 || off + len > nbases);
+  const bool oob = p < n && (off < 0 || off + len > nbases);
   const bool live = p < n && !oob;
   if (!live) off = 0;
   uint32_t anybad = 0u;
-  uint2* out = reinterpret_cast<uint2*>(packed);
+  uint4* dst = reinterpret_cast<uint4*>(packed + tile * (int64_t)len * 64);
   for (int c0 = 0; c0 < len; c0 += 32) {
     const int nb = len - c0 < 32 ? len - c0 : 32;
     const uint32_t vm = nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u);
     uint32_t xh = 0u, xl = 0u;
     if (live) {
-      xh = plane_bits(hi, off + c0) & vm;
-      xl = plane_bits(lo, off + c0) & vm;
-      anybad |= plane_bits(bad, off + c0) & vm;
+      uint32_t xb;
+      window_bits(planes, off + c0, xh, xl, xb);
+      xh &= vm;
+      xl &= vm;
+      anybad |= xb & vm;
     }
     const uint32_t yh = warp_transpose32(xh, lane);
     const uint32_t yl = warp_transpose32(xl, lane);
-    if (lane < nb) out[(tile * len + c0 + lane) * 32 + gl] = make_uint2(yh, yl);
+    stage[lane][warp] = make_uint2(yh, yl);
+    __syncthreads();
+    // nb positions x 256 bytes = nb * 16 uint4, contiguous from position c0
+    const uint4* src = reinterpret_cast<const uint4*>(&stage[0][0]);
+    for (int t = threadIdx.x; t < nb * 16; t += 1024) dst[(int64_t)c0 * 16 + t] = src[t];
+    __syncthreads();
   }
   const uint32_t u = __ballot_sync(0xFFFFFFFFu, anybad != 0u || oob);
   if (lane == 0) undef[g] = u;
 }
 
-int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int len, int64_t stride, uint32_t* hi,
-                       uint32_t* lo, uint32_t* bad, cudaStream_t stream) {
+int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int len, int64_t stride,
+                       uint32_t* planes, cudaStream_t stream) {
   const int64_t total = n_rows * (int64_t)len;
   const int64_t nwords = (total + 31) / 32 + 1;  // + 1: the funnel shift's look-ahead word
   int64_t blocks = (nwords + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  pack_planes_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rows, n_rows, len, stride, hi, lo, bad,
-                                                           nwords);
+  pack_planes_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rows, n_rows, len, stride,
+                                                           reinterpret_cast<uint4*>(planes), nwords);
   return 0;
 }
 
-int launch_gather_windows(const uint32_t* hi, const uint32_t* lo, const uint32_t* bad,
-                          int64_t nbases, const int64_t* offsets, int64_t n, int len,
-                          uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
-  const int64_t ngroups_total = (n + 1023) / 1024 * 32;  // whole tiles (zero-filled tail)
-  const int64_t blocks = (ngroups_total + 3) / 4;
-  gather_windows_kernel<<<(unsigned)blocks, 128, 0, stream>>>(hi, lo, bad, nbases, offsets, n, len,
-                                                              packed, undef, ngroups_total);
+int launch_gather_windows(const uint32_t* planes, int64_t nbases, const int64_t* offsets, int64_t n,
+                          int len, uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
+  const int64_t tiles = (n + 1023) / 1024;  // whole tiles (zero-filled tail)
+  gather_windows_kernel<<<(unsigned)tiles, 1024, 0, stream>>>(
+      reinterpret_cast<const uint4*>(planes), nbases, offsets, n, len, packed, undef);
   return 0;
 }
 

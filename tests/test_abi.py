@@ -93,13 +93,15 @@ def test_argument_validation_before_any_launch(lib):
     assert lib.gk_accuracy(P, 1, P, 100, P, 100, P, 2, P, None) == -1       # bits stride
     assert lib.gk_accuracy(P, 4, P, 100, P, 100, P, 0, P, None) == 0
     assert lib.gk_plane_words(0) == 1 and lib.gk_plane_words(33) == 3
-    assert lib.gk_pack_planes(P, 1, 0, 10, P, P, P, None) == -2
-    assert lib.gk_pack_planes(P, 1, 100, 10, P, P, P, None) == -1     # stride < len
-    assert lib.gk_pack_planes(P, 0, 100, 100, None, None, None, None) == 0
-    assert lib.gk_gather_windows(P, P, P, 1000, P, 10, 0, P, P, None) == -2
-    assert lib.gk_gather_windows(P, P, P, 1000, P + 4, 10, 100, P, P, None) == -4  # offsets
-    assert lib.gk_gather_windows(P, P, P, 1000, P, 10, 100, P + 8, P, None) == -4  # packed
-    assert lib.gk_gather_windows(P, P, P, 1000, None, 10, 100, P, P, None) == -1
+    assert lib.gk_pack_planes(P, 1, 0, 10, P, None) == -2
+    assert lib.gk_pack_planes(P, 1, 100, 10, P, None) == -1     # stride < len
+    assert lib.gk_pack_planes(P, 1, 100, 100, P + 4, None) == -4
+    assert lib.gk_pack_planes(P, 0, 100, 100, None, None) == 0
+    assert lib.gk_gather_windows(P, 1000, P, 10, 0, P, P, None) == -2
+    assert lib.gk_gather_windows(P, 1000, P + 4, 10, 100, P, P, None) == -4  # offsets
+    assert lib.gk_gather_windows(P, 1000, P, 10, 100, P + 8, P, None) == -4  # packed
+    assert lib.gk_gather_windows(P + 8, 1000, P, 10, 100, P, P, None) == -4  # planes
+    assert lib.gk_gather_windows(P, 1000, None, 10, 100, P, P, None) == -1
     assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 1 << 30, 1000) == -1  # chunk
     assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 10, 1024) == -5
     import ctypes as C

@@ -1,7 +1,7 @@
 """Small invocation of every kernel of libgk.so, for compute-sanitizer runs
 (memcheck / racecheck / synccheck / initcheck): TMA encoder + tail paths, the
 register filter, the block-transposed filter and its e sweep, the mask-major fallback, the fused
-ASCII filter, compaction (single and batched), the accuracy harness and the host
+ASCII filter, compaction (single and batched), the reference-index packing / gathering, the accuracy harness and the host
 pipelines."""
 import os
 import sys
@@ -26,6 +26,9 @@ for L, n in [(100, 3000), (150, 2200), (37, 1500)]:
         gk.filter_sweep(q, s, uq, us, n, L, e)
         gk.filter_ascii(r, f, e, L)
         gk.compact(acc, n)
+    gp = gk.pack_planes(f)
+    offs = torch.arange(n, device="cuda", dtype=torch.int64) * L
+    gk.gather_windows(gp, n * L, offs, L)
     d = gk.edit_distance(r, f, L)
     a2, e2 = gk.filter_sweep(q, s, uq, us, n, L, 4)
     gk.accuracy(a2, e2, d, n, range(5))
