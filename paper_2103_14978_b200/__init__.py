@@ -17,7 +17,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgk.so")
+LIB_PATH = os.environ.get("GK_LIB", os.path.join(HERE, "libgk.so"))
 GK_MAX_LEN = 508
 GK_MAX_STRIDE = 1024
 GK_TILE = 1024
