@@ -207,6 +207,82 @@ __device__ __forceinline__ void encode_quad(const RowAddr<SM4>& ra, int q, int r
     if (m < rem) emit(q, m, hb[m], hb[m] ^ lb[m]);  // paper code: high = b2, low = b1^b2
 }
 
+// Sparse last quad iteration (NIT >= 2, R <= 16 quads left, e.g. 6 at 150 bp):
+// instead of R lanes doing whole quads while 32-R idle, P lanes share a quad,
+// each encoding 32/P of its rows (P = 2, 4, 8); the P partial words of a
+// position are OR-combined with shuffles.  Rows are addressed at run time
+// (row p*32/P + r of the lane's part), any alignment (two LDS + funnel shift).
+// Returns the lane's undefined rows as a row bit mask (bit s = row s).
+template <int SM4, int P, bool LPART, uint32_t OFF, typename Emit>
+__device__ __forceinline__ uint32_t encode_tail(const RowAddr<SM4>& ra, int q0, int R, int len,
+                                                uint32_t& anybad, Emit&& emit) {
+  constexpr int RP = 32 / P;  // rows per part
+  constexpr int NB = RP / 4;  // 4-row blocks per part
+  const int lane = threadIdx.x & 31;
+  const int qi = lane / P, part = lane % P;
+  const int q = q0 + qi;
+  const bool valid = qi < R;
+  const uint32_t buf = ra.a[0] - 4u * (uint32_t)lane;
+  const uint32_t stride = ra.a[1] - ra.a[0] + (uint32_t)(SM4 & 3);
+  const int rem = len - 4 * q;
+  bool pm[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) pm[m] = m < rem;
+  uint32_t hb[4] = {0u, 0u, 0u, 0u}, lb[4] = {0u, 0u, 0u, 0u}, badj[NB];
+#pragma unroll
+  for (int j = NB - 1; j >= 0; --j) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t srow = (uint32_t)(part * RP + 4 * j + k);
+      const uint32_t a = buf + OFF + srow * stride + 4u * (uint32_t)(valid ? q : q0);
+      uint32_t lo, hi;
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(lo) : "r"(a & ~3u));
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(hi) : "r"((a & ~3u) + 4u));
+      w[k] = __funnelshift_r(lo, hi, (a & 3u) * 8u);
+    }
+    const uint32_t t0 = __byte_perm(w[0], w[1], 0x5140);
+    const uint32_t t1 = __byte_perm(w[0], w[1], 0x7362);
+    const uint32_t t2 = __byte_perm(w[2], w[3], 0x5140);
+    const uint32_t t3 = __byte_perm(w[2], w[3], 0x7362);
+    uint32_t r[4];
+    r[0] = __byte_perm(t0, t2, 0x5410);
+    r[1] = __byte_perm(t0, t2, 0x7632);
+    r[2] = __byte_perm(t1, t3, 0x5410);
+    r[3] = __byte_perm(t1, t3, 0x7632);
+    uint32_t bad = 0u;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      uint32_t x = r[m];
+      if (LPART) x = pm[m] ? x : 0x41414141u;
+      bad = acc_invalid(bad, x);
+      hb[m] = __funnelshift_l(gather_bit2(x), hb[m], 4);
+      lb[m] = lb[m] * 16u + __umulhi(gather_bit1(x), 16u);
+    }
+    badj[j] = valid ? bad : 0u;
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    uint32_t h = hb[m] << (part * RP), l = lb[m] << (part * RP);
+#pragma unroll
+    for (int d = 1; d < P; d <<= 1) {
+      h |= __shfl_xor_sync(0xFFFFFFFFu, h, d);
+      l |= __shfl_xor_sync(0xFFFFFFFFu, l, d);
+    }
+    if (valid && part == 0 && m < rem) emit(q, m, h, h ^ l);
+  }
+  uint32_t rows = 0u;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    anybad |= badj[j];
+    const uint32_t b = badj[j];
+    const uint32_t nz = ((b & 0x7F7F7F7Fu) + 0x7F7F7F7Fu | b) & 0x80808080u;
+    const uint32_t nib = (nz >> 7 & 1u) | (nz >> 14 & 2u) | (nz >> 21 & 4u) | (nz >> 28 & 8u);
+    rows |= nib << (part * RP + 4 * j);
+  }
+  return rows;
+}
+
 // Encode all quads of the lane for the staged group at buffer offset BOFF
 // (compile-time, like the quad offsets: the 32 row addresses stay in registers
 // and every LDS uses an immediate offset).
@@ -219,9 +295,23 @@ __device__ __forceinline__ uint32_t encode_group_v2(const RowAddr<SM4>& ra, int 
   uint32_t bad[8];
 #pragma unroll
   for (int b = 0; b < 8; ++b) bad[b] = 0u;
+  uint32_t tail_rows = 0u, tail_any = 0u;
 #pragma unroll
   for (int it = 0; it < NIT; ++it) {
     const int q = lane + 32 * it;
+    const int R = nquads - 32 * it;  // quads left for this iteration (warp-uniform)
+    if (NIT >= 2 && it == NIT - 1 && R <= 16) {
+      constexpr uint32_t TOFF = BOFF;
+      if (R <= 0) {
+      } else if (R <= 4) {
+        tail_rows = encode_tail<SM4, 8, LPART, TOFF>(ra, 32 * it, R, len, tail_any, emit);
+      } else if (R <= 8) {
+        tail_rows = encode_tail<SM4, 4, LPART, TOFF>(ra, 32 * it, R, len, tail_any, emit);
+      } else {
+        tail_rows = encode_tail<SM4, 2, LPART, TOFF>(ra, 32 * it, R, len, tail_any, emit);
+      }
+      continue;
+    }
     if (q < nquads) {
       const int rem = len - 4 * q;
       if (it == 0) encode_quad<SM4, LPART, BOFF>(ra, q, rem, bad, emit);
@@ -233,12 +323,12 @@ __device__ __forceinline__ uint32_t encode_group_v2(const RowAddr<SM4>& ra, int 
   // undefined bases are rare (0.3% of pairs in the paper's Set_3, Table S.1
   // :509): one warp-wide OR decides whether the per-row flags are needed at all
   {
-    uint32_t any = 0u;
+    uint32_t any = tail_any;
 #pragma unroll
     for (int blk = 0; blk < 8; ++blk) any |= bad[blk];
     if (__reduce_or_sync(0xFFFFFFFFu, any) == 0u) return 0u;
   }
-  uint32_t und = 0u;
+  uint32_t und = __reduce_or_sync(0xFFFFFFFFu, tail_rows);
 #pragma unroll
   for (int blk = 0; blk < 8; ++blk) {
     const uint32_t b = __reduce_or_sync(0xFFFFFFFFu, bad[blk]);
