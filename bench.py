@@ -638,6 +638,9 @@ def measure_e2e(gk, torch, dev, n, L, es, rank, world, args):
         dt = float(t.item())
     value = n_e2e * len(es) * world / dt / 1e9
     return {"value": round(value, 4), "unit": "Gpairs/s",
+            "h2d_GB_s": round(2 * n_e2e * L / dt / 1e9, 1),
+            "note": "bound by the host->device copy of the ASCII pairs (PCIe Gen5 x16, ~55-60 GB/s "
+                    "pinned); the device work of a step is ~4 ms of the ~110 ms",
             "h2d_bytes_per_step": 2 * n_e2e * L,
             "d2h_bytes_per_step": (n_e2e // 8 + n_e2e) * len(es),
             "api": "gk_filter_host_sweep (pinned host buffers; each chunk copied + encoded once, "

@@ -208,6 +208,25 @@ int gk_gather_windows(const uint32_t* d_planes, int64_t n_bases, const int64_t* 
                       int64_t n_pairs, int32_t len, uint32_t* d_packed, uint32_t* d_undef,
                       void* stream);
 
+/* Index mode from HOST candidate lists (the mapper-facing end-to-end call):
+ * the read and genome planes are resident on the device (gk_pack_planes);
+ * per chunk only the two int64 offsets of each pair cross PCIe (16 bytes per
+ * pair instead of 2*len ASCII bytes), are gathered into the packed layout and
+ * filtered for every e <= e_max in one sweep pass; the result rows come back.
+ *  h_read_offsets, h_ref_offsets : n_pairs int64 base offsets (host memory;
+ *                                  pinned for full PCIe bandwidth).
+ *  h_accept_bits : (e_max+1) rows of gk_result_words(n_pairs) u32 (host, written).
+ *  h_errcount    : (e_max+1) rows of n_pairs bytes (host, written) or NULL.
+ *  d_ws          : gk_host_index_workspace_bytes(chunk_pairs, len, e_max) bytes,
+ *                  256-byte aligned; chunk_pairs a multiple of 1024.
+ * Synchronous.  Errors: as gk_gather_windows + GK_ERR_E, GK_ERR_WORKSPACE. */
+size_t gk_host_index_workspace_bytes(int64_t chunk_pairs, int32_t len, int32_t e_max);
+int gk_filter_host_index(const uint32_t* d_read_planes, int64_t read_bases,
+                         const uint32_t* d_ref_planes, int64_t ref_bases,
+                         const int64_t* h_read_offsets, const int64_t* h_ref_offsets,
+                         int64_t n_pairs, int32_t len, int32_t e_max, uint32_t* h_accept_bits,
+                         uint8_t* h_errcount, void* d_ws, size_t ws_bytes, int64_t chunk_pairs);
+
 /* Accuracy harness: the ground truth of the paper's
  * accuracy study -- exact global edit distance, as Edlib in global mode
  * -- and the false-accept / false-reject tallies of filter

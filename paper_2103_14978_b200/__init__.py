@@ -60,6 +60,9 @@ def load_library(path: str = LIB_PATH):
         "gk_compact_rows_workspace_bytes": (SZ, [I64, I32]),
         "gk_edit_distance": (ctypes.c_int, [P, P, I64, I64, I32, P, P]),
         "gk_plane_words": (SZ, [I64]),
+        "gk_host_index_workspace_bytes": (SZ, [I64, I32, I32]),
+        "gk_filter_host_index": (ctypes.c_int, [P, I64, P, I64, P, P, I64, I32, I32, P, P, P, SZ,
+                                                I64]),
         "gk_pack_planes": (ctypes.c_int, [P, I64, I32, I64, P, P]),
         "gk_gather_windows": (ctypes.c_int, [P, I64, P, I64, I32, P, P, P]),
         "gk_accuracy": (ctypes.c_int, [P, I64, P, I64, P, I64, P, I32, P, P]),
@@ -255,6 +258,29 @@ def gather_windows(planes, n_bases: int, offsets, length: int, out=None, stream=
                                             _stream(stream)),
            "gk_gather_windows")
     return packed, undef
+
+
+def filter_host_index(read_planes, read_bases: int, ref_planes, ref_bases: int, read_offsets,
+                      ref_offsets, length: int, e_max: int, accept=None, errcount=None,
+                      workspace=None, chunk_pairs: int = 1 << 21):
+    """Index mode from HOST int64 offset tensors (planes on the device) -> host result
+    rows (accept bits [e_max+1, words], errcount [e_max+1, n] or None)."""
+    import torch
+    n = read_offsets.numel()
+    if accept is None:
+        accept = torch.empty((e_max + 1, max(1, result_words(n))), dtype=torch.int32,
+                             pin_memory=True)
+    if workspace is None:
+        workspace = torch.empty(load_library().gk_host_index_workspace_bytes(chunk_pairs, length,
+                                                                             e_max),
+                                dtype=torch.uint8, device=read_planes.device)
+    _check(load_library().gk_filter_host_index(read_planes.data_ptr(), read_bases,
+                                               ref_planes.data_ptr(), ref_bases,
+                                               read_offsets.data_ptr(), ref_offsets.data_ptr(), n,
+                                               length, e_max, accept.data_ptr(), _ptr(errcount),
+                                               workspace.data_ptr(), workspace.numel(),
+                                               chunk_pairs), "gk_filter_host_index")
+    return accept, errcount
 
 
 # ---- accuracy harness (not on the filtering path) ------------------------------

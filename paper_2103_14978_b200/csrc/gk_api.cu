@@ -418,4 +418,93 @@ int gk_filter_host_sweep(const uint8_t* h_reads, const uint8_t* h_refs, int64_t 
   return rc;
 }
 
+// ---- host-buffer index mode ----------------------------------------------------
+static size_t index_chunk_bytes(int64_t chunk, int32_t len, int32_t e_max) {
+  const size_t offs = round_up((size_t)chunk * 16, 256);
+  const size_t packed = round_up(gk_packed_words(chunk, len) * 4, 256);
+  const size_t undef = round_up(gk_undef_words(chunk) * 4, 256);
+  const size_t acc = round_up((size_t)(chunk / 32) * 4, 256);
+  const size_t err = round_up((size_t)chunk, 256);
+  return offs + 2 * packed + 2 * undef + (size_t)(e_max + 1) * (acc + err);
+}
+
+size_t gk_host_index_workspace_bytes(int64_t chunk_pairs, int32_t len, int32_t e_max) {
+  if (chunk_pairs <= 0 || len <= 0 || e_max < 0) return 0;
+  return 2 * index_chunk_bytes(chunk_pairs, len, e_max);
+}
+
+int gk_filter_host_index(const uint32_t* d_read_planes, int64_t read_bases,
+                         const uint32_t* d_ref_planes, int64_t ref_bases,
+                         const int64_t* h_read_offsets, const int64_t* h_ref_offsets,
+                         int64_t n_pairs, int32_t len, int32_t e_max, uint32_t* h_accept_bits,
+                         uint8_t* h_errcount, void* d_ws, size_t ws_bytes, int64_t chunk_pairs) {
+  if (n_pairs < 0 || read_bases < 0 || ref_bases < 0) return GK_ERR_ARG;
+  if (len < 1 || len > GK_MAX_LEN) return GK_ERR_LEN;
+  if (e_max < 0 || e_max >= len) return GK_ERR_E;
+  if (n_pairs == 0) return GK_OK;
+  if (!d_read_planes || !d_ref_planes || !h_read_offsets || !h_ref_offsets || !h_accept_bits)
+    return GK_ERR_ARG;
+  if (chunk_pairs <= 0 || chunk_pairs % 1024 != 0) return GK_ERR_ARG;
+  if (!d_ws || ws_bytes < gk_host_index_workspace_bytes(chunk_pairs, len, e_max))
+    return GK_ERR_WORKSPACE;
+  if (!aligned(d_ws, 256) || !aligned(d_read_planes, 16) || !aligned(d_ref_planes, 16))
+    return GK_ERR_ALIGN;
+  const size_t per_set = index_chunk_bytes(chunk_pairs, len, e_max);
+  const size_t words_total = gk_result_words(n_pairs);
+  cudaStream_t st[2];
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t err = cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking);
+    if (err != cudaSuccess) {
+      if (b == 1) cudaStreamDestroy(st[0]);
+      return cuda_status(err);
+    }
+  }
+  int rc = GK_OK;
+  const int64_t nchunks = (n_pairs + chunk_pairs - 1) / chunk_pairs;
+  for (int64_t c = 0; c < nchunks && rc == GK_OK; ++c) {
+    const int b = (int)(c & 1);
+    uint8_t* base = static_cast<uint8_t*>(d_ws) + b * per_set;
+    int64_t* d_roff = reinterpret_cast<int64_t*>(base);
+    int64_t* d_foff = d_roff + chunk_pairs;
+    uint32_t* pq = reinterpret_cast<uint32_t*>(base + round_up((size_t)chunk_pairs * 16, 256));
+    uint32_t* pr = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(pq) +
+                                               round_up(gk_packed_words(chunk_pairs, len) * 4, 256));
+    uint32_t* uq = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(pr) +
+                                               round_up(gk_packed_words(chunk_pairs, len) * 4, 256));
+    uint32_t* ur = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(uq) +
+                                               round_up(gk_undef_words(chunk_pairs) * 4, 256));
+    uint8_t* outs = reinterpret_cast<uint8_t*>(ur) + round_up(gk_undef_words(chunk_pairs) * 4, 256);
+    const int64_t p0 = c * chunk_pairs;
+    const int64_t np = (n_pairs - p0) < chunk_pairs ? (n_pairs - p0) : chunk_pairs;
+    cudaError_t err = cudaMemcpyAsync(d_roff, h_read_offsets + p0, (size_t)np * 8,
+                                      cudaMemcpyHostToDevice, st[b]);
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(d_foff, h_ref_offsets + p0, (size_t)np * 8, cudaMemcpyHostToDevice,
+                            st[b]);
+    if (err != cudaSuccess) { rc = cuda_status(err); break; }
+    gk::launch_gather_windows(d_read_planes, read_bases, d_roff, np, len, pq, uq, st[b]);
+    gk::launch_gather_windows(d_ref_planes, ref_bases, d_foff, np, len, pr, ur, st[b]);
+    const size_t words = (size_t)((np + 31) / 32);
+    uint32_t* acc = reinterpret_cast<uint32_t*>(outs);
+    uint8_t* ec = h_errcount ? outs + (size_t)(e_max + 1) * round_up((size_t)(chunk_pairs / 32) * 4, 256)
+                             : nullptr;
+    gk::launch_filter_sweep(pq, pr, uq, ur, np, len, e_max, acc, ec, 0, st[b]);
+    rc = after_launch();
+    for (int e = 0; e <= e_max && rc == GK_OK; ++e) {
+      err = cudaMemcpyAsync(h_accept_bits + (size_t)e * words_total + p0 / 32, acc + (size_t)e * words,
+                            words * 4, cudaMemcpyDeviceToHost, st[b]);
+      if (err == cudaSuccess && h_errcount)
+        err = cudaMemcpyAsync(h_errcount + (size_t)e * n_pairs + p0, ec + (size_t)e * np, (size_t)np,
+                              cudaMemcpyDeviceToHost, st[b]);
+      if (err != cudaSuccess) rc = cuda_status(err);
+    }
+  }
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t err = cudaStreamSynchronize(st[b]);
+    if (rc == GK_OK && err != cudaSuccess) rc = cuda_status(err);
+    cudaStreamDestroy(st[b]);
+  }
+  return rc;
+}
+
 }  // extern "C"

@@ -102,6 +102,10 @@ def test_argument_validation_before_any_launch(lib):
     assert lib.gk_gather_windows(P, 1000, P, 10, 100, P + 8, P, None) == -4  # packed
     assert lib.gk_gather_windows(P + 8, 1000, P, 10, 100, P, P, None) == -4  # planes
     assert lib.gk_gather_windows(P, 1000, None, 10, 100, P, P, None) == -1
+    assert lib.gk_host_index_workspace_bytes(1024, 100, 10) > 2 * 1024 * 16
+    assert lib.gk_filter_host_index(P, 10, P, 10, P, P, 10, 100, 100, P, None, P, 1 << 30, 1024) == -3
+    assert lib.gk_filter_host_index(P, 10, P, 10, P, P, 10, 100, 5, P, None, P, 1 << 30, 1000) == -1
+    assert lib.gk_filter_host_index(P, 10, P, 10, P, P, 10, 100, 5, P, None, P, 10, 1024) == -5
     assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 1 << 30, 1000) == -1  # chunk
     assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 10, 1024) == -5
     import ctypes as C

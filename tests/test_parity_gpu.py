@@ -328,6 +328,24 @@ def test_reference_index_mode(gk, L, emax):
         assert bad.size == 0, (L, e, bad[:5])
 
 
+def test_filter_host_index(gk):
+    """Host candidate lists through gk_filter_host_index (3 chunks) == the device
+    index path == the oracle."""
+    L, emax, G = 100, 8, 300_007
+    genome, reads, read_id, pos = make_index_case(G, 2000, 5000, L, seed=21)
+    gp = gk.pack_planes(to_dev(genome.reshape(1, -1)))
+    rp = gk.pack_planes(to_dev(reads))
+    ro = torch.from_numpy(read_id * L).pin_memory()
+    fo = torch.from_numpy(pos).pin_memory()
+    err = torch.empty((emax + 1, 5000), dtype=torch.uint8).pin_memory()
+    acc, _ = gk.filter_host_index(rp, 2000 * L, gp, G, ro, fo, L, emax, errcount=err,
+                                  chunk_pairs=2048)
+    oa, oc = oracle.sweep(reads[read_id], np.stack([genome[p:p + L] for p in pos]), emax)
+    for e in range(emax + 1):
+        assert (unpack_accept(acc[e], 5000) == oa[e]).all(), e
+        assert (err[e].numpy() == oc[e]).all(), e
+
+
 def test_reference_index_out_of_range_windows(gk):
     L, G = 50, 10_000
     genome, reads, read_id, pos = make_index_case(G, 100, 2100, L, seed=5)

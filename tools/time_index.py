@@ -75,6 +75,23 @@ same = torch.equal(uq, uq2) and torch.equal(ur, ur2)
 acc2, err2 = gk.filter_sweep(q2, r2, uq2, ur2, a.cands, a.L, a.emax)
 torch.cuda.synchronize()
 same = same and torch.equal(acc, acc2) and torch.equal(err, err2)
+# end to end from host candidate lists (offsets in pinned host memory, results back to host)
+import time  # noqa: E402
+ro_h = roff.cpu().pin_memory()
+fo_h = pos.cpu().pin_memory()
+acc_h = torch.empty((a.emax + 1, gk.result_words(a.cands)), dtype=torch.int32, pin_memory=True)
+err_h = torch.empty((a.emax + 1, a.cands), dtype=torch.uint8, pin_memory=True)
+chunk = 1 << 21
+ws = torch.empty(gk.load_library().gk_host_index_workspace_bytes(chunk, a.L, a.emax),
+                 dtype=torch.uint8, device="cuda")
+gk.filter_host_index(rp, a.reads * a.L, gp, a.G, ro_h, fo_h, a.L, a.emax, accept=acc_h,
+                     errcount=err_h, workspace=ws, chunk_pairs=chunk)
+t0 = time.perf_counter()
+for _ in range(3):
+    gk.filter_host_index(rp, a.reads * a.L, gp, a.G, ro_h, fo_h, a.L, a.emax, accept=acc_h,
+                         errcount=err_h, workspace=ws, chunk_pairs=chunk)
+dt_e2e = (time.perf_counter() - t0) / 3
+same = same and torch.equal(acc_h.cuda(), acc) and torch.equal(err_h.cuda(), err)
 gbytes = a.cands * (3 * a.L / 8 + a.L / 4 + 1 / 8)  # planes of the window + packed words out
 print(json.dumps({
     "G": a.G, "reads": a.reads, "cands": a.cands, "L": a.L, "emax": a.emax,
@@ -87,4 +104,7 @@ print(json.dumps({
     "ms_encode_ascii_path": round(ms_encode, 4),
     "ascii_path_Gfiltrations_s": round(a.cands * (a.emax + 1) / (ms_encode + ms_sweep) / 1e6, 2),
     "ascii_input_bytes_per_pair": 2 * a.L, "index_input_bytes_per_pair": 16,
+    "e2e_host_index_s": round(dt_e2e, 4),
+    "e2e_host_index_Gfiltrations_s": round(a.cands * (a.emax + 1) / dt_e2e / 1e9, 2),
+    "e2e_h2d_bytes": a.cands * 16, "e2e_d2h_bytes": (a.emax + 1) * (a.cands // 8 + a.cands),
     "results_identical_to_ascii_path": bool(same)}), flush=True)
