@@ -327,10 +327,12 @@ struct NoHook {
 
 // Threshold sweep: F_e of every e <= e_max is a prefix
 // of the same AND chain, so one pass counts all of them.  The counter of F_k
-// (8 bit-sliced planes, CsaCounter layout) lives in shared memory,
-// [k-1][8][32 lanes]: bank = lane, conflict-free.
+// (NP bit-sliced planes, NP = the bits of the largest count 2*ceil(L/4): 6 at
+// 100 bp, 7 at 150 / 250 bp) lives in shared memory, [k-1][NP][32 lanes]:
+// bank = lane, conflict-free.
 // Out of line: the 13-step unrolled chunk would otherwise carry 13 copies of
 // the counting code (instruction-cache pressure, measured: stall_no_instruction).
+template <int NP>
 __device__ __noinline__ void sweep_count(uint32_t* p, uint32_t f0, uint32_t f1, uint32_t f2,
                                          uint32_t f3, uint32_t f4, uint32_t f5, uint32_t f6,
                                          uint32_t f7) {
@@ -345,25 +347,37 @@ __device__ __noinline__ void sweep_count(uint32_t* p, uint32_t f0, uint32_t f1, 
   st[5] = f5 & ~f4;
   st[6] = f6 & ~f5;
   st[7] = f7 & ~f6;
-  CsaCounter c;
-  c.ones = p[0];
-  c.twos = p[32];
-  c.fours = p[64];
+  uint32_t ones = p[0], twos = p[32], fours = p[64], up[NP - 3];
 #pragma unroll
-  for (int b = 0; b < 5; ++b) c.up[b] = p[(3 + b) * 32];
-  c.add8(st);
-  p[0] = c.ones;
-  p[32] = c.twos;
-  p[64] = c.fours;
+  for (int b = 0; b < NP - 3; ++b) up[b] = p[(3 + b) * 32];
+  // carry-save tree: 7 full adders, then the weight-8 carry ripples upwards
+  uint32_t c0, c1, c2, c3, d0, d1, f;
+  CsaCounter::fa(ones, st[0], st[1], c0);
+  CsaCounter::fa(ones, st[2], st[3], c1);
+  CsaCounter::fa(ones, st[4], st[5], c2);
+  CsaCounter::fa(ones, st[6], st[7], c3);
+  CsaCounter::fa(twos, c0, c1, d0);
+  CsaCounter::fa(twos, c2, c3, d1);
+  CsaCounter::fa(fours, d0, d1, f);
 #pragma unroll
-  for (int b = 0; b < 5; ++b) p[(3 + b) * 32] = c.up[b];
+  for (int b = 0; b < NP - 3; ++b) {
+    const uint32_t t = up[b] & f;
+    up[b] ^= f;
+    f = t;
+  }
+  p[0] = ones;
+  p[32] = twos;
+  p[64] = fours;
+#pragma unroll
+  for (int b = 0; b < NP - 3; ++b) p[(3 + b) * 32] = up[b];
 }
 
+template <int NP>
 struct SweepHook {
   static constexpr bool kSweep = true;
   uint32_t* sm;  // this warp's counters, already offset by lane
   __device__ __forceinline__ void operator()(int k, const uint32_t (&F)[B]) const {
-    sweep_count(sm + (k - 1) * 8 * 32, F[0], F[1], F[2], F[3], F[4], F[5], F[6], F[7]);
+    sweep_count<NP>(sm + (k - 1) * NP * 32, F[0], F[1], F[2], F[3], F[4], F[5], F[6], F[7]);
   }
 };
 
@@ -417,6 +431,7 @@ void launch_bt(const uint2* reads, const uint2* refs, const uint32_t* rund, cons
 // decision for e uses c0 (the Hamming-stage count, readings R5/R9) and count(F_e).
 constexpr int SWEEP_WARPS = 2;
 
+template <int NP>
 __global__ void __launch_bounds__(SWEEP_WARPS * 32, 6) filter_bt_sweep_kernel(
     const uint2* __restrict__ reads, const uint2* __restrict__ refs,
     const uint32_t* __restrict__ rund, const uint32_t* __restrict__ fund, int64_t n, int len,
@@ -427,8 +442,8 @@ __global__ void __launch_bounds__(SWEEP_WARPS * 32, 6) filter_bt_sweep_kernel(
   const int64_t tile = (int64_t)blockIdx.x * SWEEP_WARPS + warp;
   const int64_t g = tile * 32 + lane;
   if (tile * 1024 >= n) return;
-  uint32_t* mine = sm_sweep + (size_t)warp * emax * 8 * 32 + lane;
-  for (int j = 0; j < emax * 8; ++j) mine[j * 32] = 0u;
+  uint32_t* mine = sm_sweep + (size_t)warp * emax * NP * 32 + lane;
+  for (int j = 0; j < emax * NP; ++j) mine[j * 32] = 0u;
   const uint2* q = reads + tile * (int64_t)len * 32 + lane;
   const uint2* r = refs + tile * (int64_t)len * 32 + lane;
   CsaCounter cA, cF;
@@ -442,7 +457,7 @@ __global__ void __launch_bounds__(SWEEP_WARPS * 32, 6) filter_bt_sweep_kernel(
     R.h[c] = v.x;
     R.l[c] = v.y;
   }
-  const bt::SweepHook hook{mine};
+  const bt::SweepHook<NP> hook{mine};
 #pragma unroll 1
   for (int ib = 0; ib < len; ib += bt::B) {
     bt::block(q, r, R, ib, len, emax, edge_fix, cA, cF, aprev, fprev, hook);
@@ -458,27 +473,39 @@ __global__ void __launch_bounds__(SWEEP_WARPS * 32, 6) filter_bt_sweep_kernel(
 #pragma unroll
       for (int b = 0; b < 8; ++b) f[b] = a[b];
     } else {
-      const uint32_t* p = mine + (e - 1) * 8 * 32;
+      const uint32_t* p = mine + (e - 1) * NP * 32;
 #pragma unroll
-      for (int b = 0; b < 8; ++b) f[b] = p[b * 32];
+      for (int b = 0; b < 8; ++b) f[b] = b < NP ? p[b * 32] : 0u;
     }
     finish_group(a, f, e, und, g, n, accept + e * words, errc ? errc + e * n : nullptr);
   }
 }
 
-size_t sweep_smem_bytes(int emax) { return (size_t)SWEEP_WARPS * emax * 8 * 32 * 4; }
+template <int NP>
+static void launch_sweep_np(const uint2* reads, const uint2* refs, const uint32_t* rund,
+                            const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,
+                            uint8_t* errc, int edge_fix, cudaStream_t stream) {
+  const int64_t tiles = (n + 1023) / 1024;
+  const int64_t blocks = (tiles + SWEEP_WARPS - 1) / SWEEP_WARPS;
+  const size_t smem = (size_t)SWEEP_WARPS * emax * NP * 32 * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(filter_bt_sweep_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  filter_bt_sweep_kernel<NP><<<(unsigned)blocks, SWEEP_WARPS * 32, smem, stream>>>(
+      reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix);
+}
 
 void launch_bt_sweep(const uint2* reads, const uint2* refs, const uint32_t* rund,
                      const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,
                      uint8_t* errc, int edge_fix, cudaStream_t stream) {
-  const int64_t tiles = (n + 1023) / 1024;
-  const int64_t blocks = (tiles + SWEEP_WARPS - 1) / SWEEP_WARPS;
-  const size_t smem = sweep_smem_bytes(emax);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(filter_bt_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  filter_bt_sweep_kernel<<<(unsigned)blocks, SWEEP_WARPS * 32, smem, stream>>>(
-      reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix);
+  // counter planes: enough bits for the largest count, 2 * ceil(len / 4) (R6, R7)
+  const int maxc = 2 * ((len + 3) / 4);
+  if (maxc < 64)
+    launch_sweep_np<6>(reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix, stream);
+  else if (maxc < 128)
+    launch_sweep_np<7>(reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix, stream);
+  else
+    launch_sweep_np<8>(reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix, stream);
 }
 
 }  // namespace gk
