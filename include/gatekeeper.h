@@ -136,8 +136,11 @@ int gk_filter_ex(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
  *                  threshold e, bit p%32 of word p/32 (written).
  *  d_errcount    : (e_max+1) rows of n_pairs bytes, row e (written) or NULL.
  *  flags         : 0 or GK_FLAG_NO_EDGE_FIX (original GateKeeper).
- * Same inputs, alignment and ownership as gk_filter.  Errors: GK_ERR_ARG,
- * GK_ERR_LEN, GK_ERR_E (e_max outside [0, len)), GK_ERR_ALIGN, GK_ERR_CUDA. */
+ * Same inputs, alignment and ownership as gk_filter.  (Beyond ~100
+ * thresholds the per-e counters no longer fit in shared memory and the rows
+ * come from one gk_filter launch per e: same results, no one-pass speed-up.)
+ * Errors: GK_ERR_ARG, GK_ERR_LEN, GK_ERR_E (e_max outside [0, len)),
+ * GK_ERR_ALIGN, GK_ERR_CUDA. */
 int gk_filter_sweep(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
                     const uint32_t* d_read_undef, const uint32_t* d_ref_undef,
                     int64_t n_pairs, int32_t len, int32_t e_max,

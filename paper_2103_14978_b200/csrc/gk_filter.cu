@@ -164,8 +164,21 @@ void launch_bt_sweep(const uint2* reads, const uint2* refs, const uint32_t* rund
 int launch_filter_sweep(const uint32_t* reads, const uint32_t* refs, const uint32_t* rund,
                         const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,
                         uint8_t* errc, int flags, cudaStream_t stream) {
-  launch_bt_sweep(reinterpret_cast<const uint2*>(reads), reinterpret_cast<const uint2*>(refs),
-                  rund, fund, n, len, emax, accept, errc, (flags & 2) ? 0 : 1, stream);
+  // the one-pass kernel keeps emax counters of up to 8 planes per warp in shared
+  // memory (2 warps per CTA): beyond ~100 thresholds they no longer fit, and the
+  // rows are produced by one gk_filter launch per e instead (same results)
+  const int maxc = 2 * ((len + 3) / 4);
+  const int np = maxc < 64 ? 6 : (maxc < 128 ? 7 : 8);
+  const size_t smem = (size_t)2 * emax * np * 32 * 4;
+  if (smem <= 200 * 1024) {
+    launch_bt_sweep(reinterpret_cast<const uint2*>(reads), reinterpret_cast<const uint2*>(refs),
+                    rund, fund, n, len, emax, accept, errc, (flags & 2) ? 0 : 1, stream);
+    return 0;
+  }
+  const int64_t words = (n + 31) / 32;
+  for (int e = 0; e <= emax; ++e)
+    launch_filter(reads, refs, rund, fund, n, len, e, accept + e * words,
+                  errc ? errc + e * n : nullptr, flags & 2, stream);
   return 0;
 }
 

@@ -240,6 +240,17 @@ def test_sweep_kernel_adversarial_and_ragged(gk):
         assert_sweep_parity(gk, reads, refs, 12)
 
 
+def test_sweep_many_thresholds_fallback(gk):
+    """e_max beyond the one-pass kernel's shared-memory counters (here 299 at
+    300 bp): gk_filter_sweep falls back to one filter launch per e -- same rows."""
+    L, emax = 300, 299
+    reads, refs = pairgen.gen_pairs(600, L, profile=pairgen.PROFILE_BALANCED, emax=40, seed=3)
+    a, c = run_sweep(gk, reads, refs, emax)
+    oa, oc = oracle.sweep(reads, refs, emax)
+    for e in range(0, emax + 1, 23):
+        assert (a[e] == oa[e]).all() and (c[e] == oc[e]).all(), e
+
+
 @pytest.mark.parametrize("L", [17, 100])
 def test_sweep_kernel_original_gatekeeper(gk, L):
     reads, refs = pairgen.gen_pairs(2000, L, profile=pairgen.PROFILE_BALANCED, emax=L // 10 + 1,
