@@ -129,8 +129,12 @@ def load_traffic(workload):
         except (OSError, ValueError):
             continue
         if d.get("workload") == workload:
-            best = {k.split("(")[0].strip(): int(v["traffic_bytes_per_launch"])
-                    for k, v in d.get("kernels", {}).items()}
+            best = {}
+            for k, v in d.get("kernels", {}).items():
+                name = k.split("(")[0].strip()
+                best[name] = int(v["traffic_bytes_per_launch"])
+                # a templated kernel is also found by its base name
+                best.setdefault(name.split("<")[0].strip(), best[name])
     return best
 
 

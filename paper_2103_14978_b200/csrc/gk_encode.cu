@@ -25,6 +25,10 @@
 #ifndef GK_ENCODE_TMA
 #define GK_ENCODE_TMA 1
 #endif
+// minimum resident CTAs per SM requested from ptxas for the TMA encoder (A/B knob)
+#ifndef GK_ENC_MINB
+#define GK_ENC_MINB 1
+#endif
 
 namespace gk {
 
@@ -83,7 +87,7 @@ __global__ void encode_tail_kernel(int64_t first_group, int64_t end_group, int l
 // block's span being prefetched while the current one is encoded.  The 4 groups'
 // words are collected in shared memory and written out as full 32-byte sectors.
 template <int PMAX, int SM4, bool LPART>
-__global__ void __launch_bounds__(128) encode_tma_kernel(const uint8_t* __restrict__ seqs,
+__global__ void __launch_bounds__(128, GK_ENC_MINB) encode_tma_kernel(const uint8_t* __restrict__ seqs,
                                                          int64_t nblocks, int len, int stride,
                                                          uint32_t* __restrict__ packed,
                                                          uint32_t* __restrict__ undef) {

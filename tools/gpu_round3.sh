@@ -15,7 +15,7 @@ timeout 600 python bench.py --config c4 --no-e2e --no-cpu-baseline > gpurun_out/
 timeout 900 python bench.py --config c5 --steps 3 --warmup 3 > gpurun_out/bench_c5_${TAG}.json 2> gpurun_out/bench_c5_${TAG}.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-alt > gpurun_out/bench_under_ncu_${TAG}.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"filter_bt_sweep|encode_tma|compact" -c 4 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"filter_bt_sweep|encode_tma|compact" -c 5 \
     -o gpurun_out/prof_bench_${TAG} python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-alt > gpurun_out/ncu_bench_${TAG}.log 2>&1
 tail -n 2 gpurun_out/ncu_bench_${TAG}.log
 head -c 700 gpurun_out/bench_c2_${TAG}.json
