@@ -430,9 +430,13 @@ void launch_bt(const uint2* reads, const uint2* refs, const uint32_t* rund, cons
 // each block runs to e_max and the hook counts F_k after every step; the
 // decision for e uses c0 (the Hamming-stage count, readings R5/R9) and count(F_e).
 constexpr int SWEEP_WARPS = 2;
+// minimum resident CTAs per SM requested from ptxas for the sweep (A/B knob)
+#ifndef GK_SWEEP_MINB
+#define GK_SWEEP_MINB 6
+#endif
 
 template <int NP>
-__global__ void __launch_bounds__(SWEEP_WARPS * 32, 6) filter_bt_sweep_kernel(
+__global__ void __launch_bounds__(SWEEP_WARPS * 32, GK_SWEEP_MINB) filter_bt_sweep_kernel(
     const uint2* __restrict__ reads, const uint2* __restrict__ refs,
     const uint32_t* __restrict__ rund, const uint32_t* __restrict__ fund, int64_t n, int len,
     int emax, uint32_t* __restrict__ accept, uint8_t* __restrict__ errc, int edge_fix) {
