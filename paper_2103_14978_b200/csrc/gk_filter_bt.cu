@@ -432,7 +432,7 @@ void launch_bt(const uint2* reads, const uint2* refs, const uint32_t* rund, cons
 constexpr int SWEEP_WARPS = 2;
 // minimum resident CTAs per SM requested from ptxas for the sweep (A/B knob)
 #ifndef GK_SWEEP_MINB
-#define GK_SWEEP_MINB 6
+#define GK_SWEEP_MINB 5
 #endif
 
 template <int NP>
