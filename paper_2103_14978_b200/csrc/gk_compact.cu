@@ -11,6 +11,12 @@
 
 namespace gk {
 
+// GK_COMPACT_STAGED=1 (default): shared-memory-staged index writes; 0: the
+// earlier shuffle loop with direct global stores (A/B knob)
+#ifndef GK_COMPACT_STAGED
+#define GK_COMPACT_STAGED 1
+#endif
+
 constexpr int CP_THREADS = 256;
 constexpr int CP_WORDS_PER_THREAD = 8;
 constexpr int CP_WORDS_PER_CTA = CP_THREADS * CP_WORDS_PER_THREAD;  // 65536 pairs
@@ -111,6 +117,37 @@ __global__ void __launch_bounds__(CP_THREADS) compact_write_kernel(
   // warp start offset = exclusive prefix of lane 0 of this warp
   const uint32_t warp_off = __shfl_sync(0xFFFFFFFFu, before, 0);
   unsigned long long o = sm_base + warp_off;
+#if GK_COMPACT_STAGED
+  // staged variant: per 32-word chunk each lane expands its own word's set bits
+  // (ffs loop) into the warp's shared-memory slice at its scanned offset, then
+  // the warp copies the chunk's run out with coalesced stores
+  __shared__ uint32_t stage[CP_THREADS / 32][1024];
+  if (idx != nullptr) {
+    uint32_t* st = stage[warp];
+#pragma unroll 1
+    for (int t = 0; t < CP_WORDS_PER_THREAD; ++t) {
+      uint32_t w = words[t];
+      const uint32_t c = __popc(w);
+      uint32_t x = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+        if (lane >= d) x += y;
+      }
+      const uint32_t tot = __shfl_sync(0xFFFFFFFFu, x, 31);
+      uint32_t pos = x - c;
+      const uint32_t base = (uint32_t)((wbase + 32 * t + lane) * 32);
+      while (w) {
+        st[pos++] = base + (uint32_t)(__ffs(w) - 1);
+        w &= w - 1u;
+      }
+      __syncwarp();
+      for (uint32_t j = lane; j < tot; j += 32) idx[o + j] = st[j];
+      __syncwarp();
+      o += tot;
+    }
+  }
+#else
   if (idx != nullptr) {
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
@@ -125,6 +162,7 @@ __global__ void __launch_bounds__(CP_THREADS) compact_write_kernel(
       }
     }
   }
+#endif
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *n_acc = sm_base + total;
 }
 
