@@ -418,7 +418,8 @@ def main():
     def entry(kernel, bound, ach, peak, unit, launch_ms, share, extra):
         d = {"bound": bound, "achieved": round(ach, 3), "peak": round(peak, 3), "unit": unit,
              "frac": round(ach / peak, 4), "kernel": kernel,
-             "traffic": traffic.get(kernel) if traffic else None,
+             "traffic": (traffic.get(kernel, traffic.get(kernel.split("<")[0].strip()))
+                         if traffic else None),
              "peak_source": peak_src if unit == "GB/s" else
              f"derived: 148 SM x 64 ALU lanes/clk x {clk_mhz:.0f} MHz (DESIGN.md section 6)",
              "mean_launch_ms": round(launch_ms, 4), "share_of_step": round(share, 4)}
@@ -440,7 +441,7 @@ def main():
                              tot_ms / ms_per_step, fextra))
     if args.path in ("packed", "sweep"):
         enc_bytes_launch = n * L + n * L / 4 + n / 8
-        kernels.append(entry("encode_tma_kernel<128, 0, 0>" if L <= 128 else "encode_tma_kernel",
+        kernels.append(entry("encode_tma_kernel<128, 0, 0, 1>" if L <= 128 else "encode_tma_kernel",
                              "hbm", enc_bytes_launch / (enc_ms / 2 / 1e3) / 1e9, hbm_peak, "GB/s",
                              enc_ms / 2, enc_ms / ms_per_step,
                              {"api": "gk_encode (2 launches per step: reads, reference segments)",

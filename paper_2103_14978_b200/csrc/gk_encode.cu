@@ -29,6 +29,13 @@
 #ifndef GK_ENC_MINB
 #define GK_ENC_MINB 1
 #endif
+// The 256-byte staging variant runs at 3 CTAs per SM (168 registers) when its last
+// lane-iteration is the sparse shared-quad tail (len <= 192, e.g. 150 bp: 1.63 ->
+// 1.54 ms per 30M) and at the register-unbounded 2 CTAs per SM otherwise (250 bp:
+// 3 CTAs measured 2.11 -> 2.19 ms); profiles/r01l_encoder_wide_minb_ab.jsonl.
+#ifndef GK_ENC_MINB_SPARSE
+#define GK_ENC_MINB_SPARSE 3
+#endif
 
 namespace gk {
 
@@ -86,8 +93,8 @@ __global__ void encode_tail_kernel(int64_t first_group, int64_t end_group, int l
 // of 32*stride bytes) arrive by one cp.async.bulk into a double buffer, the next
 // block's span being prefetched while the current one is encoded.  The 4 groups'
 // words are collected in shared memory and written out as full 32-byte sectors.
-template <int PMAX, int SM4, bool LPART>
-__global__ void __launch_bounds__(128, GK_ENC_MINB) encode_tma_kernel(const uint8_t* __restrict__ seqs,
+template <int PMAX, int SM4, bool LPART, int MB>
+__global__ void __launch_bounds__(128, MB) encode_tma_kernel(const uint8_t* __restrict__ seqs,
                                                          int64_t nblocks, int len, int stride,
                                                          uint32_t* __restrict__ packed,
                                                          uint32_t* __restrict__ undef) {
@@ -151,7 +158,11 @@ static void launch_tma(const uint8_t* seqs, int64_t nblocks, int len, int stride
                        uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
   const int nq = (len + 3) >> 2;
   const size_t smem = (size_t)4 * 2 * 32 * PMAX + (size_t)2 * 16 * 8 * nq + 64;
-  auto kern = encode_tma_kernel<PMAX, SM4, LPART>;
+  constexpr int MB = PMAX == 128 ? GK_ENC_MINB : 1;
+  constexpr int MB_SPARSE = PMAX == 256 ? GK_ENC_MINB_SPARSE : MB;
+  const bool sparse_tail = PMAX == 256 && nq - 32 <= 16;  // NIT = 2, R <= 16 quads
+  auto kern = sparse_tail ? encode_tma_kernel<PMAX, SM4, LPART, MB_SPARSE>
+                          : encode_tma_kernel<PMAX, SM4, LPART, MB>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 148, per_sm = 1;
