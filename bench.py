@@ -1,20 +1,28 @@
 #!/usr/bin/env python
 """bench.py -- throughput of the GateKeeper-GPU hot path on B200 (one JSON line).
 
-Default (N=1): BASELINE.json configs[1] -- 30M synthetic pairs of 100 bp, error
-threshold swept e = 0..10.  One step = the whole hot path (SURVEY.md 8(a)
-a1..a7) over the batch for every e of the sweep: gk_encode of the reads and of
-the reference segments (a1, independent of e, once per step), then per e
-gk_filter (a2..a6: Hamming / shifted masks, amendment, edge fix, AND, windowed
-count, decision) and gk_compact (a7: ordered indices of the accepted pairs).
---path fused runs gk_filter_ascii (a1..a6 in one kernel, re-encoding for every
-e) + gk_compact instead.  The metric is filtrations per second (pairs x
-thresholds / s), in G pairs/s.
+Default: BASELINE.json configs[4] (the config the metric is quoted on): 1B
+synthetic pairs, a 100/150/250 bp mix with e = 5% of L (5 / 7 / 12), split
+evenly over the ranks (strong scaling: the job is fixed, N GPUs share it).
+One step = the whole hot path over the rank's share of
+every length bucket: the fused ASCII filtration (gk_filter_ascii: a1 encode,
+a2 undefined pass, a3-a6 masks / amend / edge fix / AND / count / decision)
+and a7 compaction (gk_compact: the ordered indices of the accepted pairs).
+Inputs are generated on the device (pairgen) and resident in HBM when a timed
+region starts; a share that does not fit the memory budget runs as resident
+chunks whose device times add up (the paper's kernel-time method).
+value = 1B pairs / (max over ranks of the device time of one step).
 
-Multi-GPU (torchrun, one process per GPU): every rank filters its own shard of
-the same size (weak scaling, no collective on the data path); time = max over
-ranks of the device time; an NCCL all-reduce of the accepted-pair totals runs
-after the timed region only.
+--config c2|c3|c4 (BASELINE configs[1..3], 30M pairs per GPU, e swept
+0..e_max, weak scaling): one step = gk_encode x2 + gk_filter_sweep (every e in
+one pass) + gk_compact_rows; value = filtrations/s (pairs x thresholds).
+
+Multi-GPU: `python bench.py --gpus N` re-launches itself under
+torch.distributed.run (one process per GPU, NCCL); the driver's own torchrun
+launch is used as is.  No collective touches the data path; the max over
+ranks of the device time and the accepted-pair totals are all-reduced after
+the timed region (PAPER.md:79 equal batches, :186 slowest device).
+--dry-run exercises that orchestration on CPU with gloo and no kernels.
 
 --impl reference: the CPU oracle (oracle/), as it stands, timed on this host's
 cores on a bounded sample of the same workload (rank 0 only).
@@ -24,6 +32,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,38 +41,109 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIGS = {
-    # name: (n_pairs per GPU, read length, e values, BASELINE configs index)
-    "c2": (30_000_000, 100, list(range(0, 11)), 1),
-    "c3": (30_000_000, 150, list(range(0, 16)), 2),
-    "c4": (30_000_000, 250, list(range(0, 26)), 3),
+from pairgen.workloads import SEED, WORKLOADS  # noqa: E402
+
+METRIC = "filtered pairs/sec (Gpairs/s)"
+
+# the paper's own filtering throughput for the same path, with its GPUs named
+# (BASELINE.md; kernel time, 30M real pairs per length; M pairs/s)
+PAPER = {
+    "c5": {"note": "PAPER.md reports no 1B-pair mix; nearest: GTX 1080 Ti (Pascal), 1 GPU, kernel "
+                   "throughput at e=4 (150 bp) / e=5 (100 bp) / e=10 (250 bp, closest to 12)",
+           "gpu": "1x NVIDIA GeForce GTX 1080 Ti (Setup_1)",
+           "Mpairs_s": {"100bp_e5_host_encoded": 103.9, "100bp_e5_device_encoded": 62.8,
+                        "150bp_e4_host_encoded": 85.5, "150bp_e4_device_encoded": 37.1,
+                        "250bp_e10_host_encoded": 25.7, "250bp_e10_device_encoded": 16.0},
+           "multi_gpu": "8x GTX 1080 Ti: 100 bp e=2 1.333 G pairs/s host-encoded, 0.496 device-encoded "
+                        "(Table S.21 :892-899)",
+           "source": "Tables S.17-S.19 PAPER.md:815-857"},
+    "c2": {"gpu": "1x NVIDIA GeForce GTX 1080 Ti", "Mpairs_s_per_e_host_encoded":
+           {"0": 699.7, "1": 282.6, "2": 198.7, "3": 149.7, "4": 122.5, "5": 103.9, "6": 89.7},
+           "source": "Table S.17 PAPER.md:815-821"},
+    "c3": {"gpu": "1x NVIDIA GeForce GTX 1080 Ti", "Mpairs_s_per_e_host_encoded":
+           {"0": 537.7, "1": 193.5, "2": 138.6, "4": 85.5, "6": 62.1, "8": 48.4, "10": 40.8},
+           "source": "Table S.18 PAPER.md:831-837"},
+    "c4": {"gpu": "1x NVIDIA GeForce GTX 1080 Ti", "Mpairs_s_per_e_host_encoded":
+           {"0": 328.2, "1": 132.2, "2": 92.0, "4": 56.5, "6": 40.6, "8": 31.2, "10": 25.7},
+           "source": "Table S.19 PAPER.md:851-857"},
 }
-BASE_SEED = 2103149780
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c5"])
-    p.add_argument("--total", type=int, default=1_000_000_000,
-                   help="c5: total pairs over all ranks (the 100/150/250 bp mix)")
-    p.add_argument("--mem-gb", type=float, default=100.0,
-                   help="c5: device memory budget for resident inputs per rank")
-    p.add_argument("--path", default="sweep", choices=["sweep", "packed", "fused"],
-                   help="sweep: gk_encode x2 + gk_filter_sweep (all e in one pass); packed: "
-                        "gk_encode x2 + gk_filter per e; fused: gk_filter_ascii per e")
-    p.add_argument("--no-alt", action="store_true",
-                   help="skip the extra timing of the per-e packed path")
-    p.add_argument("--n", type=int, default=None, help="override pairs per GPU")
+    p.add_argument("--config", default="c5", choices=["c2", "c3", "c4", "c5"])
+    p.add_argument("--path", default=None,
+                   help="c5: fused (default) | packed;  c2-c4: sweep (default) | packed | fused")
+    p.add_argument("--total", type=int, default=None, help="c5: total pairs (default 1B)")
+    p.add_argument("--n", type=int, default=None, help="c2-c4: pairs per GPU (default 30M)")
+    p.add_argument("--mem-gb", type=float, default=110.0,
+                   help="device memory budget for one resident chunk of pairs")
+    p.add_argument("--dry-run", action="store_true",
+                   help="CPU/gloo: exercise spawning, sharding and the rank reductions only")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-sample", type=int, default=None)
-    return p.parse_args()
+    p.add_argument("--no-alt", action="store_true", help="c2-c4: skip the per-e comparison path")
+    p.add_argument("--cpu-budget", type=float, default=20.0,
+                   help="seconds of host work for the oracle baseline")
+    a = p.parse_args(argv)
+    if a.path is None:
+        a.path = "fused" if a.config == "c5" else "sweep"
+    return a
 
 
+# ---------------------------------------------------------------------------
+# workload description shared by both arms (the driver compares the configs)
+def buckets_of(args):
+    """[(L, es, idx0, n_total)] of the workload."""
+    wl = WORKLOADS[args.config]
+    if args.config == "c5":
+        if args.total is None:
+            return [(b.L, b.es, b.idx0, b.n) for b in wl.buckets]
+        out, start = [], 0
+        for i, b in enumerate(wl.buckets):
+            n = args.total // 3 + (1 if i < args.total % 3 else 0)
+            out.append((b.L, b.es, start, n))
+            start += n
+        return out
+    b = wl.buckets[0]
+    return [(b.L, b.es, 0, args.n or b.n)]
+
+
+def config_of(args, world):
+    wl = WORKLOADS[args.config]
+    bk = buckets_of(args)
+    if args.config == "c5":
+        total = sum(b[3] for b in bk)
+        return {"workload": f"c5: {total} pairs, 100/150/250 bp thirds, e = 5/7/12 "
+                            f"(BASELINE configs[{wl.config_index}]), split evenly over the ranks",
+                "total_pairs": total,
+                "buckets": [{"read_len": L, "e": es[0], "pairs": n} for L, es, _, n in bk],
+                "path": {"fused": "gk_filter_ascii + gk_compact per bucket",
+                         "packed": "gk_encode x2 + gk_filter + gk_compact per bucket"}[args.path],
+                "profile": "paper", "seed": SEED,
+                "l2": "inputs >= 6.6 GB per resident chunk > 126 MB L2 (no flush needed)",
+                "parallelism": f"dp{world} (pairs sharded, no data-path collective)"}
+    L, es, _, n = bk[0]
+    return {"workload": f"{args.config}: {n} pairs x {L} bp per GPU, e swept {es[0]}..{es[-1]} "
+                        f"(BASELINE configs[{wl.config_index}])",
+            "n_pairs_per_gpu": n, "read_len": L, "e": f"{es[0]}-{es[-1]}",
+            "path": {"fused": "gk_filter_ascii + gk_compact per e",
+                     "packed": "gk_encode x2 + (gk_filter + gk_compact) per e",
+                     "sweep": "gk_encode x2 + gk_filter_sweep + gk_compact_rows (all e)"}[args.path],
+            "profile": "paper", "seed": SEED,
+            "l2": f"inputs {2 * n * L / 1e9:.1f} GB per GPU > 126 MB L2 (no flush needed)",
+            "parallelism": f"dp{world} (pairs sharded, no data-path collective)"}
+
+
+def unit_of(args):
+    return "Gpairs/s" if args.config == "c5" else "G filtrations/s (pairs x thresholds)"
+
+
+# ---------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -79,7 +159,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -111,15 +191,31 @@ class ClockSampler:
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f), "measured"
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
     except OSError:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(workload):
-    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
-    kernels of this workload, from the newest committed ncu --set full capture
-    (profiles/r*_traffic.json, written by tools/ncu_traffic.py); None if absent."""
+def int_peak():
+    """Integer-pipe peaks measured live on this GPU (tools/native/int_peak.cu):
+    thread-instructions/s of LOP3 / IADD3 / SHF / PRMT (alu pipe), IMAD (fma pipe)."""
+    import ctypes
+    so = os.path.join(ROOT, "tools", "native", "libint_peak.so")
+    if not os.path.exists(so):
+        return None
+    lib = ctypes.CDLL(so)
+    lib.ip_measure.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.ip_measure.restype = ctypes.c_int
+    out = (ctypes.c_double * 6)()
+    if lib.ip_measure(ctypes.cast(out, ctypes.c_void_p), 5) != 0:
+        return None
+    names = ["lop3", "iadd3", "shf", "prmt", "imad", "lop3+imad"]
+    return {k: round(v / 1e12, 3) for k, v in zip(names, out)}
+
+
+def load_ncu(workload):
+    """Per-launch DRAM traffic and ALU-pipe utilisation of this workload's kernels from
+    the newest committed ncu --set full capture (profiles/r*_traffic.json)."""
     import glob
     best = None
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json"))):
@@ -132,525 +228,453 @@ def load_traffic(workload):
             best = {}
             for k, v in d.get("kernels", {}).items():
                 name = k.split("(")[0].strip()
-                best[name] = int(v["traffic_bytes_per_launch"])
-                # a templated kernel is also found by its base name
-                best.setdefault(name.split("<")[0].strip(), best[name])
+                best[name] = v
+                best.setdefault(name.split("<")[0].strip(), v)
     return best
 
 
-def cpu_baseline(cfg_name, sample_pairs=None, budget_s=15.0):
-    """The oracle, as it stands, on this host's cores over a bounded sample."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+# ---------------------------------------------------------------------------
+# the oracle on the host cores
+def oracle_rate(L, es, sample, threads):
+    """Seconds per pair of the oracle (all thresholds es) on `sample` pairs."""
     import oracle
     import pairgen
-    n_full, L, es, _ = CONFIGS[cfg_name]
-    cores = os.cpu_count() or 1
-    sample = sample_pairs
-    if sample is None:
-        # calibrate: ~budget_s of CPU work over the e sweep
-        probe = 2000
-        r, f = pairgen.gen_pairs(probe, L)
-        t0 = time.perf_counter()
-        for e in es:
-            oracle.filter(r, f, e, nthreads=cores)
-        dt = time.perf_counter() - t0
-        sample = int(max(1024, min(n_full, probe * budget_s / max(dt, 1e-6))))
-    r, f = pairgen.gen_pairs(sample, L)
+    r, f = pairgen.gen_pairs(sample, L, nthreads=os.cpu_count() or 1)
     t0 = time.perf_counter()
-    for e in es:
-        oracle.filter(r, f, e, nthreads=cores)
-    dt = time.perf_counter() - t0
-    value = sample * len(es) / dt / 1e9
-    return {"value": value, "unit": "Gpairs/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {sample} pairs of the {n_full}-pair {L} bp batch, e = {es[0]}..{es[-1]}, "
-                      f"{dt:.1f} s wall on {cores} threads"}
+    if len(es) == 1:
+        oracle.filter(r, f, es[0], nthreads=threads)
+    else:
+        for e in es:
+            oracle.filter(r, f, e, nthreads=threads)
+    return (time.perf_counter() - t0) / sample
+
+
+def cpu_baseline(args, budget_s):
+    """The oracle, as it stands, on this host's cores over a bounded sample of every bucket
+    (T = nproc and T = 1), scaled to the whole workload."""
+    cores = os.cpu_count() or 1
+    bk = buckets_of(args)
+    per_bucket = budget_s / len(bk)
+    t_all, t_one, desc = 0.0, 0.0, []
+    for L, es, _, n in bk:
+        probe = oracle_rate(L, es, 1024, cores)
+        sample = int(max(1024, min(n, 0.8 * per_bucket / max(probe, 1e-12))))
+        tp = oracle_rate(L, es, sample, cores)
+        s1 = int(max(256, min(sample, 0.2 * per_bucket / max(probe * cores, 1e-12))))
+        tp1 = oracle_rate(L, es, s1, 1)
+        t_all += n * tp
+        t_one += n * tp1
+        desc.append(f"{sample} pairs at {L} bp (T={cores}), {s1} (T=1)")
+    work = sum(n * len(es) for _, es, _, n in bk)
+    return {"value": work / t_all / 1e9, "unit": unit_of(args), "cores": cores, "kind": "oracle",
+            "value_1thread": work / t_one / 1e9, "cpu_model": cpu_model(),
+            "sample": "; ".join(desc) + f"; scaled to the workload's {work} filtrations",
+            "api": "oracle.filter (oracle/gk_oracle.c, plain character-level C, one call per e)"}
 
 
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the oracle on the host cores, each step a bounded sample."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    n_full, L, es, cidx = CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    bk = buckets_of(args)
+    total_steps = args.steps + args.warmup
+    per_step = 150.0 / total_steps / len(bk)  # ~2.5 min for the whole run
+    samples = []
+    for L, es, _, n in bk:
+        probe = oracle_rate(L, es, 1024, cores)
+        samples.append(int(max(1024, min(n, per_step / max(probe, 1e-12)))))
     import oracle
     import pairgen
-    cores = os.cpu_count() or 1
-    # bounded sample per step so that warmup + steps end within a few minutes
-    probe = 2000
-    r, f = pairgen.gen_pairs(probe, L)
-    t0 = time.perf_counter()
-    for e in es:
-        oracle.filter(r, f, e, nthreads=cores)
-    per_pair = (time.perf_counter() - t0) / probe
-    total_steps = args.steps + args.warmup
-    sample = int(max(1024, min(n_full, 120.0 / total_steps / max(per_pair, 1e-9))))
-    r, f = pairgen.gen_pairs(sample, L)
+    data = [pairgen.gen_pairs(s, L, nthreads=cores) for (L, _, _, _), s in zip(bk, samples)]
+
+    def step():
+        t = []
+        for (L, es, _, n), (r, f) in zip(bk, data):
+            t0 = time.perf_counter()
+            for e in es:
+                oracle.filter(r, f, e, nthreads=cores)
+            t.append(time.perf_counter() - t0)
+        return t
+
     for _ in range(args.warmup):
-        for e in es:
-            oracle.filter(r, f, e, nthreads=cores)
-    t0 = time.perf_counter()
+        step()
+    acc = [0.0] * len(bk)
     for _ in range(args.steps):
-        for e in es:
-            oracle.filter(r, f, e, nthreads=cores)
-    dt = time.perf_counter() - t0
-    value = sample * len(es) * args.steps / dt / 1e9
+        for i, x in enumerate(step()):
+            acc[i] += x
+    # seconds per pair per bucket -> the whole workload's time per step
+    t_work = sum(n * acc[i] / args.steps / samples[i] for i, (_, _, _, n) in enumerate(bk))
+    work = sum(n * len(es) for _, es, _, n in bk)
+    value = work / t_work / 1e9
+    sample = ", ".join(f"{s} pairs at {L} bp" for (L, _, _, _), s in zip(bk, samples))
     line = {
-        "impl": "reference", "metric": "filtered pairs/sec (Gpairs/s)", "value": value,
-        "unit": "Gpairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt * 1000 / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {n_full} pairs x {L} bp, e {es[0]}..{es[-1]} "
-                               f"(BASELINE configs[{cidx}]); each step a {sample}-pair sample",
-                   "read_len": L, "e": f"{es[0]}-{es[-1]}", "profile": "paper", "seed": BASE_SEED},
-        "cpu_baseline": {"value": value, "unit": "Gpairs/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{sample} pairs per step x {len(es)} thresholds"},
-        "e2e": {"value": value, "unit": "Gpairs/s", "h2d_bytes_per_step": 0,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": unit_of(args),
+        "n_gpus": int(os.environ.get("WORLD_SIZE", args.gpus)), "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_work * 1e3, "higher_is_better": True,
+        "scaling": "strong" if args.config == "c5" else "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic",
+        "config": config_of(args, int(os.environ.get("WORLD_SIZE", args.gpus))),
+        "cpu_baseline": {"value": value, "unit": unit_of(args), "cores": cores, "kind": "oracle",
+                         "cpu_model": cpu_model(),
+                         "sample": f"each step: {sample}; time scaled to the whole workload"},
+        "e2e": {"value": value, "unit": unit_of(args), "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-launch under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """CPU / gloo: spawning, sharding and the rank reductions, no kernels."""
+    import torch.distributed as dist
+
+    from paper_2103_14978_b200 import sharding
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    shards = []
+    for L, es, idx0, n in buckets_of(args):
+        lo, cnt = (sharding.even_shard(n, rank, world) if args.config == "c5"
+                   else sharding.weak_shard(n, rank))
+        shards.append([L, idx0 + lo, cnt])
+    counts = sharding.sum_over_ranks([s[2] for s in shards])
+    tmax = sharding.max_over_ranks(float(rank + 1))
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": unit_of(args), "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "dry_run": True,
+                          "scaling": "strong" if args.config == "c5" else "weak",
+                          "config": config_of(args, world), "rank0_shards": shards,
+                          "pairs_all_ranks": counts, "max_over_ranks_of_rank_plus_1": tmax}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per pair (DESIGN.md section 6)
+def alg_bytes(kernel, L, es):
+    rows = len(es)
+    return {"filter_ascii": 2 * L + 1 / 8 + 1,
+            "encode": 2 * (L + L / 4) + 2 / 8,
+            "filter": L / 2 + 2 / 8 + 1 / 8 + 1,
+            "filter_sweep": L / 2 + 2 / 8 + rows * (1 / 8 + 1),
+            "compact": rows * 2 / 8,       # + 4 B per accepted pair, added by the caller
+            "compact_rows": rows * 2 / 8}[kernel]
+
+
+def alg_ops(kernel, L, es):
+    """Method-minimum integer ops per pair on bit-sliced words: 5 LOP3 per (position, mask)
+    cell (2 mismatch + 3 amend/AND), 4 per position per counted bit-vector (start detect +
+    carry-save add), over 32 pairs per word."""
+    e = max(es)
+    cells = L * (2 * e + 1) - e * (e + 1)
+    if kernel in ("filter", "filter_ascii"):
+        return (5 * cells + 8 * L) / 32.0
+    if kernel == "filter_sweep":
+        return (5 * cells + 4 * L * (e + 2)) / 32.0
+    return 0.0
+
+
+# ---------------------------------------------------------------------------
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if args.dry_run:
+        run_dry(args)
+        return
 
     import torch
     import torch.distributed as dist
 
-    import pairgen
     import paper_2103_14978_b200 as gk
     from paper_2103_14978_b200 import sharding
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (use --dry-run on CPU)")
+    dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     gk.load_library()
-
-    if args.config == "c5":
-        run_c5(args, torch, dist, pairgen, gk, sharding, world, rank, dev)
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
-    n_cfg, L, es, cidx = CONFIGS[args.config]
-    n = args.n or n_cfg
-    # this rank's shard: pairs [rank*n, (rank+1)*n) of the seeded stream
-    idx0, n = sharding.weak_shard(n, rank)
-    reads, refs = pairgen.gen_pairs_cuda(n, L, idx0=idx0, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    rows = len(es) if args.path == "sweep" else 1
-    assert es == list(range(len(es)))
-    accept = torch.empty((rows, gk.result_words(n)), dtype=torch.int32, device=dev)
-    errc = torch.empty((rows, n), dtype=torch.uint8, device=dev)
-    idx = torch.empty(n, dtype=torch.int32, device=dev)
-    n_acc = torch.zeros(len(es), dtype=torch.int64, device=dev)
-    ws = torch.empty(gk.compact_workspace_bytes(n), dtype=torch.uint8, device=dev)
-    if args.path == "sweep":
-        # a7 for every row in one launch pair: one index list per e
-        idx_rows = torch.empty((rows, n), dtype=torch.int32, device=dev)
-        ws_rows = torch.empty(gk.compact_rows_workspace_bytes(n, rows), dtype=torch.uint8,
-                              device=dev)
-    if args.path in ("packed", "sweep"):
-        pq = torch.empty(gk.packed_words(n, L), dtype=torch.int32, device=dev)
-        pr = torch.empty_like(pq)
-        uq = torch.empty(gk.undef_words(n), dtype=torch.int32, device=dev)
-        ur = torch.empty_like(uq)
-    torch.cuda.synchronize(dev)
-
-    n_ev = len(es)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_ev)]
-    ev_enc = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    enc_launches = 0
-    if args.path in ("packed", "sweep"):
-        enc_launches = 2 * (1 + (1 if n % 128 else 0) + (1 if (n + 1023) // 1024 * 32 > (n + 31) // 32 else 0))
-    if args.path == "sweep":
-        launches_per_step = 1 + 2 + enc_launches
-    else:
-        launches_per_step = len(es) * 3 + enc_launches
-
-    def step(record=False, path=args.path):
-        if path in ("packed", "sweep"):
-            if record:
-                ev_enc[0].record(stream)
-            gk.encode(reads, L, out=(pq, uq), stream=stream)
-            gk.encode(refs, L, out=(pr, ur), stream=stream)
-            if record:
-                ev_enc[1].record(stream)
-        if path == "sweep":
-            # a2-a6 for every e in one pass, then a7 per e
-            if record:
-                ev[0][0].record(stream)
-            gk.filter_sweep(pq, pr, uq, ur, n, L, es[-1], accept=accept, errcount=errc,
-                            stream=stream)
-            if record:
-                ev[0][1].record(stream)
-            gk.compact_rows(accept, n, idx=idx_rows, n_acc=n_acc, workspace=ws_rows,
-                            stream=stream)
-            if record:
-                ev[0][2].record(stream)
-            return
-        for j, e in enumerate(es):
-            if record:
-                ev[j][0].record(stream)
-            if path == "fused":
-                gk.filter_ascii(reads, refs, e, L, accept=accept[0], errcount=errc[0], stream=stream)
-            else:
-                gk.filter(pq, pr, uq, ur, n, L, e, accept=accept[0], errcount=errc[0], stream=stream)
-            if record:
-                ev[j][1].record(stream)
-            gk.compact(accept[0], n, idx=idx, n_acc=n_acc[j:j + 1], workspace=ws, stream=stream)
-            if record:
-                ev[j][2].record(stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-
-    sampler = ClockSampler(dev.index)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    sampler.start()
-    time.sleep(0.3)
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    filt_ms = [0.0] * n_ev
-    comp_ms = [0.0] * n_ev
-    t_start.record(stream)
-    for _ in range(args.steps):
-        step(record=True)
-    t_end.record(stream)
-    torch.cuda.synchronize(dev)
-    clocks = sampler.stop()
-    # kernel times of the LAST step's launches (events are reused each step)
-    n_rec = 1 if args.path == "sweep" else n_ev
-    for j in range(n_rec):
-        filt_ms[j] = ev[j][0].elapsed_time(ev[j][1])
-        comp_ms[j] = ev[j][1].elapsed_time(ev[j][2])
-    elapsed = sharding.max_over_ranks(t_start.elapsed_time(t_end), device=dev)
-    n_acc_tot = sharding.sum_over_ranks(n_acc, device=dev)
-    if world > 1:
-        dist.barrier()
-
-    # accuracy (outside the timed region): the paper's FA / FR study (Tables S.2-S.6)
-    # on the whole batch -- exact edit distance on the device (gk_edit_distance)
-    # against the sweep's decisions (gk_accuracy)
-    accuracy = None
-    if args.path == "sweep":
-        v0 = torch.cuda.Event(enable_timing=True)
-        v1 = torch.cuda.Event(enable_timing=True)
-        v0.record(stream)
-        dist = gk.edit_distance(reads, refs, L, stream=stream)
-        v1.record(stream)
-        counts = gk.accuracy(accept, errc, dist, n, es, stream=stream)
-        torch.cuda.synchronize(dev)
-        counts = sharding.sum_over_ranks(counts.flatten(), device=dev)
-        accuracy = {"verifier": "gk_edit_distance (Myers bit-vector, exact global distance)",
-                    "verifier_ms": round(v0.elapsed_time(v1), 3),
-                    "per_e": {str(e): {"accept_rate": round(counts[4 * j + 1] / max(1, counts[4 * j]), 5),
-                                       "false_accept_rate": round(counts[4 * j + 2] / max(1, counts[4 * j]), 5),
-                                       "false_rejects": int(counts[4 * j + 3])}
-                              for j, e in enumerate(es)}}
-        del dist
-
-    # the per-e packed path on the same data (context for the sweep's speed-up)
-    alt = None
-    if args.path == "sweep" and not args.no_alt:
-        for _ in range(2):
-            step(path="packed")
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(dev)
-        a0.record(stream)
-        for _ in range(3):
-            step(path="packed")
-        a1.record(stream)
-        torch.cuda.synchronize(dev)
-        alt_ms = sharding.max_over_ranks(a0.elapsed_time(a1) / 3, device=dev)
-        alt = {"path": "gk_encode x2 + (gk_filter + gk_compact) per e", "steps": 3,
-               "ms_per_step": round(alt_ms, 4),
-               "value": round(n * len(es) * world / (alt_ms / 1e3) / 1e9, 4)}
-
-    ms_per_step = elapsed / args.steps
-    filtrations = n * len(es) * world
-    value = filtrations / (ms_per_step / 1e3) / 1e9
-
-    peaks, peak_src = measured_peaks()
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    alu_peak = 148 * 64 * clk_mhz * 1e6 / 1e12  # T int-ops/s: 148 SMs x 4 SMSPs x 16 ALU lanes
-    enc_ms = ev_enc[0].elapsed_time(ev_enc[1]) if args.path in ("packed", "sweep") else 0.0
-
-    def alg_ops(e):
-        # method-minimum integer ops per pair on bit-sliced words (DESIGN.md "Roofline"):
-        # 5 LOP3 per (position, mask) cell + 8 per position for two window counters
-        cells = L * (2 * e + 1) - e * (e + 1)
-        return (5 * cells + 8 * L) / 32.0
-
-    def sweep_ops(emax):
-        # one pass: the 2*emax+1 masks once + one window counter per e (4 ops per position)
-        cells = L * (2 * emax + 1) - emax * (emax + 1)
-        return (5 * cells + 4 * L * (emax + 2)) / 32.0
-
-    if args.path == "fused":
-        bytes_launch = n * (2 * L) + n / 8 + n
-        kname = "gk_filter_ascii (filter_ascii_kernel)"
-    elif args.path == "sweep":
-        bytes_launch = n * (L / 2) + (n / 8 + n) * n_ev
-        kname = "gk_filter_sweep (filter_bt_sweep_kernel)"
-    else:
-        bytes_launch = n * (L / 2) + n / 8 + n
-        kname = "gk_filter (filter_sp_kernel<E> / filter_bt_kernel)"
-    tot_ms = sum(filt_ms)
-    n_launch = n_rec
-    hbm_ach = bytes_launch * n_launch / (tot_ms / 1e3) / 1e9
-    if args.path == "sweep":
-        alu_ach = n * sweep_ops(es[-1]) / (tot_ms / 1e3) / 1e12
-    else:
-        alu_ach = sum(n * alg_ops(e) for e in es) / (tot_ms / 1e3) / 1e12
-    traffic = load_traffic(f"{args.config}:{args.path}:{n}")
-
-    def entry(kernel, bound, ach, peak, unit, launch_ms, share, extra):
-        d = {"bound": bound, "achieved": round(ach, 3), "peak": round(peak, 3), "unit": unit,
-             "frac": round(ach / peak, 4), "kernel": kernel,
-             "traffic": (traffic.get(kernel, traffic.get(kernel.split("<")[0].strip()))
-                         if traffic else None),
-             "peak_source": peak_src if unit == "GB/s" else
-             f"derived: 148 SM x 64 ALU lanes/clk x {clk_mhz:.0f} MHz (DESIGN.md section 6)",
-             "mean_launch_ms": round(launch_ms, 4), "share_of_step": round(share, 4)}
-        d.update(extra)
-        return d
-
-    kernels = []
-    fkernel = {"fused": "filter_ascii_tma_kernel", "sweep": "filter_bt_sweep_kernel",
-               "packed": "filter_sp_kernel<E>/filter_bt_kernel"}[args.path]
-    fextra = {"api": kname, "bytes_per_launch": bytes_launch,
-              "ops_per_pair": round(sweep_ops(es[-1]) if args.path == "sweep" else
-                                    sum(alg_ops(e) for e in es) / n_ev, 2),
-              "hbm_frac": round(hbm_ach / hbm_peak, 4), "alu_frac": round(alu_ach / alu_peak, 4)}
-    if args.path == "fused" or hbm_ach / hbm_peak > alu_ach / alu_peak:
-        kernels.append(entry(fkernel, "hbm", hbm_ach, hbm_peak, "GB/s", tot_ms / n_launch,
-                             tot_ms / ms_per_step, fextra))
-    else:
-        kernels.append(entry(fkernel, "alu", alu_ach, alu_peak, "T int-ops/s", tot_ms / n_launch,
-                             tot_ms / ms_per_step, fextra))
-    if args.path in ("packed", "sweep"):
-        enc_bytes_launch = n * L + n * L / 4 + n / 8
-        kernels.append(entry("encode_tma_kernel<128, 0, 0, 1>" if L <= 128 else "encode_tma_kernel",
-                             "hbm", enc_bytes_launch / (enc_ms / 2 / 1e3) / 1e9, hbm_peak, "GB/s",
-                             enc_ms / 2, enc_ms / ms_per_step,
-                             {"api": "gk_encode (2 launches per step: reads, reference segments)",
-                              "bytes_per_launch": enc_bytes_launch}))
-    comp_tot = sum(comp_ms[:n_rec])
-    if comp_tot > 0:
-        n_claunch = 1 if args.path == "sweep" else n_ev
-        comp_bytes = (2 * (n / 8) + 4 * sum(int(x) for x in n_acc_tot) / world) / n_claunch
-        kernels.append(entry("compact_write_kernel", "hbm",
-                             comp_bytes / (comp_tot / n_claunch / 1e3) / 1e9, hbm_peak, "GB/s",
-                             comp_tot / n_claunch, comp_tot / ms_per_step,
-                             {"api": "gk_compact_rows (all e)" if args.path == "sweep"
-                              else "gk_compact per e", "bytes_per_launch": comp_bytes,
-                              "note": "count + write kernels; bytes = accept bits read twice + indices"}))
-    # the dominant kernel = the largest share of the step
-    roof = dict(max(kernels, key=lambda k: k["share_of_step"]))
-    roof["all_kernels"] = [{k: v for k, v in x.items() if k in ("kernel", "bound", "frac", "achieved",
-                                                               "unit", "share_of_step", "traffic")}
-                           for x in kernels]
-    per_e = {}
-    for j, e in enumerate(es):
-        if args.path == "sweep":
-            per_e[str(e)] = {"accepted": int(n_acc_tot[j])}
-            continue
-        t = filt_ms[j] / 1e3
-        per_e[str(e)] = {"filter_ms": round(filt_ms[j], 4), "compact_ms": round(comp_ms[j], 4),
-                         "Gpairs_s_filter": round(n / t / 1e9, 3),
-                         "hbm_frac": round(bytes_launch / t / 1e9 / hbm_peak, 4),
-                         "alu_frac": round(n * alg_ops(e) / t / 1e12 / alu_peak, 4),
-                         "accepted": int(n_acc_tot[j])}
-    if args.path == "sweep":
-        per_e["compact_ms_all_e"] = round(comp_ms[0], 4)
-    encode = None
-    if args.path in ("packed", "sweep"):
-        enc_bytes = 2 * (n * L + n * L / 4 + n / 8)
-        encode = {"ms": round(enc_ms, 4), "GB_s": round(enc_bytes / (enc_ms / 1e3) / 1e9, 1),
-                  "hbm_frac": round(enc_bytes / (enc_ms / 1e3) / 1e9 / hbm_peak, 4),
-                  "bytes": enc_bytes, "share_of_step": round(enc_ms / ms_per_step, 4)}
-
-    e2e = None
-    if not args.no_e2e:
-        e2e = measure_e2e(gk, torch, dev, n, L, es, rank, world, args)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config, args.cpu_sample)
-
+    ctx = dict(torch=torch, dist=dist, gk=gk, sharding=sharding, world=world, rank=rank, dev=dev)
+    line = run_buckets(args, ctx)
     if rank == 0:
-        line = {
-            "metric": "filtered pairs/sec (Gpairs/s)",
-            "value": round(value, 4), "unit": "Gpairs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {
-                "workload": f"{args.config}: {n} pairs x {L} bp per GPU, e swept {es[0]}..{es[-1]} "
-                            f"(BASELINE configs[{cidx}]); step = "
-                            + ("a1 once, a2-a6 for all e in one pass, a7 per e" if args.path == "sweep"
-                               else "per e: a1-a6 + a7"),
-                "n_pairs_per_gpu": n, "read_len": L, "e": f"{es[0]}-{es[-1]}",
-                "path": {"fused": "gk_filter_ascii + gk_compact per e",
-                         "packed": "gk_encode x2 + (gk_filter + gk_compact) per e",
-                         "sweep": "gk_encode x2 + gk_filter_sweep + gk_compact_rows (all e)"}[args.path],
-                "profile": "paper", "seed": BASE_SEED,
-                "l2": f"inputs {2 * n * L / 1e9:.1f} GB per GPU > 126 MB L2 (no flush needed)",
-                "parallelism": f"dp{world} (pairs sharded, no data-path collective)"},
-            "roofline": roof,
-            "encode": encode,
-            "per_e": per_e,
-            "alt_path": alt,
-            "accuracy": accuracy,
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-        }
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
-C5_BUCKETS = [(100, 5), (150, 7), (250, 12)]  # e = floor(5% of L) (BASELINE configs[4])
-
-
-def run_c5(args, torch, dist, pairgen, gk, sharding, world, rank, dev):
-    """BASELINE configs[4]: 1B pairs, a 100/150/250 bp mix with e = 5% of L, split
-    evenly over the ranks (strong scaling).  Each rank filters its third of every
-    length bucket; when its share does not fit in --mem-gb of HBM it is processed in
-    resident chunks and the time is the sum of the chunks' device times (the
-    paper's kernel-time methodology; inputs generated between chunks,
-    outside the timed spans).  One step = the rank's whole share."""
+def run_buckets(args, ctx):
+    """Time one step (every bucket of the rank's share) and build the JSON line."""
+    import pairgen
+    from paper_2103_14978_b200.pipeline import BucketStep, SweepStep
+    torch, gk, sharding = ctx["torch"], ctx["gk"], ctx["sharding"]
+    world, rank, dev = ctx["world"], ctx["rank"], ctx["dev"]
     stream = torch.cuda.current_stream(dev)
-    total = args.total
-    per_bucket = [total // 3 + (1 if b < total % 3 else 0) for b in range(3)]
-    bucket_ms = [0.0, 0.0, 0.0]
-    accepted = [0, 0, 0]
-    chunks_run = 0
-    launches = 0
-    for b, (L, e) in enumerate(C5_BUCKETS):
-        lo, cnt = sharding.even_shard(per_bucket[b], rank, world)
-        bytes_per_pair = 2 * L + L // 2 + 16
-        cap = max(1024, int(args.mem_gb * 1e9 / bytes_per_pair) // 1024 * 1024)
+    c5 = args.config == "c5"
+    bk = buckets_of(args)
+
+    # the share of this rank, in resident chunks
+    plan = []
+    for L, es, idx0, n in bk:
+        lo, cnt = sharding.even_shard(n, rank, world) if c5 else sharding.weak_shard(n, rank)
+        per_pair = 2 * L + 8 + len(es) * 6 + (L // 2 if args.path != "fused" else 0)
+        cap = max(1024, int(args.mem_gb * 1e9 / per_pair) // 1024 * 1024)
+        nch = (cnt + cap - 1) // cap
+        size = (cnt + nch - 1) // nch
+        size = (size + 1023) // 1024 * 1024
         done = 0
         while done < cnt:
-            m = min(cap, cnt - done)
-            reads, refs = pairgen.gen_pairs_cuda(m, L, idx0=lo + done, device=dev)
-            pq = torch.empty(gk.packed_words(m, L), dtype=torch.int32, device=dev)
-            pr = torch.empty_like(pq)
-            uq = torch.empty(gk.undef_words(m), dtype=torch.int32, device=dev)
-            ur = torch.empty_like(uq)
-            acc = torch.empty(gk.result_words(m), dtype=torch.int32, device=dev)
-            errc = torch.empty(m, dtype=torch.uint8, device=dev)
-            idx = torch.empty(m, dtype=torch.int32, device=dev)
-            n_acc = torch.zeros(1, dtype=torch.int64, device=dev)
-            ws = torch.empty(gk.compact_workspace_bytes(m), dtype=torch.uint8, device=dev)
-
-            def step():
-                gk.encode(reads, L, out=(pq, uq), stream=stream)
-                gk.encode(refs, L, out=(pr, ur), stream=stream)
-                gk.filter(pq, pr, uq, ur, m, L, e, accept=acc, errcount=errc, stream=stream)
-                gk.compact(acc, m, idx=idx, n_acc=n_acc, workspace=ws, stream=stream)
-
-            for _ in range(args.warmup):
-                step()
-            t0 = torch.cuda.Event(enable_timing=True)
-            t1 = torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize(dev)
-            t0.record(stream)
-            for _ in range(args.steps):
-                step()
-            t1.record(stream)
-            torch.cuda.synchronize(dev)
-            bucket_ms[b] += t0.elapsed_time(t1) / args.steps
-            accepted[b] += int(n_acc.item())
-            launches += 7 * args.steps
-            chunks_run += 1
+            m = min(size, cnt - done)
+            plan.append((L, es, idx0 + lo + done, m))
             done += m
-            del reads, refs, pq, pr, uq, ur, acc, errc, idx, ws
-            torch.cuda.empty_cache()
-    ms_rank = sum(bucket_ms)
-    ms = sharding.max_over_ranks(ms_rank, device=dev)
-    acc_tot = sharding.sum_over_ranks(accepted, device=dev)
-    value = total / (ms / 1e3) / 1e9
-    if rank == 0:
-        line = {
-            "metric": "filtered pairs/sec (Gpairs/s)", "value": round(value, 4), "unit": "Gpairs/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"c5: {total} pairs, 100/150/250 bp thirds, e = 5/7/12 "
-                                   "(BASELINE configs[4]), split evenly over the ranks",
-                       "path": "gk_encode x2 + gk_filter + gk_compact per bucket",
-                       "timing": "sum over resident chunks of CUDA-event device time; "
-                                 "max over ranks",
-                       "parallelism": f"dp{world} (pairs sharded, no data-path collective)"},
-            "per_bucket": {f"{L}bp_e{e}": {"ms_rank0": round(bucket_ms[b], 4),
-                                           "accepted": acc_tot[b]}
-                           for b, (L, e) in enumerate(C5_BUCKETS)},
-            "chunks_rank0": chunks_run, "gpu_launches": launches,
-        }
-        print(json.dumps(line), flush=True)
+
+    peaks, peak_src = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    ip = int_peak()
+    alu_peak = ip["lop3"] if ip else 148 * 64 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    alu_src = ("measured live: LOP3 chains at full occupancy (tools/native/int_peak.cu)" if ip
+               else "derived: 148 SM x 64 lanes/clk x max clock (microbenchmark unavailable)")
+
+    sampler = ClockSampler(dev.index)
+    step_ms = 0.0
+    kern_ms = {}       # kernel family -> ms per step
+    kern_work = {}     # kernel family -> (bytes, ops) per step
+    per_bucket = {}
+    accepted = {}
+    launches = 0
+    accuracy = None
+    sampler_started = False
+    for ci, (L, es, p0, m) in enumerate(plan):
+        reads, refs = pairgen.gen_pairs_cuda(m, L, idx0=p0, device=dev)
+        if c5 or args.path != "sweep":
+            steps_obj = [BucketStep(torch, m, L, e, dev, path="fused" if args.path == "fused"
+                                    else "packed") for e in es]
+        else:
+            steps_obj = [SweepStep(torch, m, L, es[-1], dev)]
+        torch.cuda.synchronize(dev)
+
+        def one(record=False):
+            for s in steps_obj:
+                s.run(reads, refs, stream, record=record)
+
+        for _ in range(args.warmup):
+            one()
+        torch.cuda.synchronize(dev)
+        if world > 1 and ci == 0:
+            ctx["dist"].barrier()
+        if not sampler_started:
+            sampler.start()
+            time.sleep(0.2)
+            sampler_started = True
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        l0 = gk.launch_count()
+        ev0.record(stream)
+        for k in range(args.steps):
+            one(record=(k == args.steps - 1))
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        launches += gk.launch_count() - l0
+        ms = ev0.elapsed_time(ev1) / args.steps
+        step_ms += ms
+        key = f"{L}bp_e{es[0]}" if c5 else f"{L}bp_e{es[0]}-{es[-1]}"
+        pb = per_bucket.setdefault(key, {"ms": 0.0, "pairs": 0, "chunks": 0})
+        pb["ms"] += ms
+        pb["pairs"] += m
+        pb["chunks"] += 1
+        for s in steps_obj:
+            for kname, kms in s.timer.ms().items():
+                kern_ms[kname] = kern_ms.get(kname, 0.0) + kms
+                kes = s.es if hasattr(s, "es") else es
+                b = alg_bytes(kname, L, kes) * m
+                if kname.startswith("compact"):
+                    b += 4 * int(s.n_acc.sum().item())
+                o = alg_ops(kname, L, kes) * m
+                w = kern_work.setdefault(kname, [0.0, 0.0, []])
+                w[0] += b
+                w[1] += o
+                w[2].append({"bucket": key, "ms": round(kms, 4), "pairs": m,
+                             "GB_s": round(b / (kms / 1e3) / 1e9, 1),
+                             "T_ops_s": round(o / (kms / 1e3) / 1e12, 3)})
+            acc_rows = s.n_acc.tolist()
+            for j, e in enumerate(s.es if hasattr(s, "es") else es):
+                accepted[f"{key}:{e}"] = accepted.get(f"{key}:{e}", 0) + int(acc_rows[j])
+        if not c5 and args.path == "sweep" and ci == len(plan) - 1:
+            # the paper's accuracy study (Tables S.2-S.6) on the whole batch, after the timed
+            # region: exact edit distance on the device vs the sweep's decisions
+            st = steps_obj[0]
+            dist_ = gk.edit_distance(reads, refs, L, stream=stream)
+            counts = gk.accuracy(st.accept, st.errc, dist_, m, es, stream=stream)
+            torch.cuda.synchronize(dev)
+            counts = sharding.sum_over_ranks(counts.flatten(), device=dev)
+            accuracy = {"verifier": "gk_edit_distance (Myers bit-vector, exact global distance)",
+                        "per_e": {str(e): {
+                            "accept_rate": round(counts[4 * j + 1] / max(1, counts[4 * j]), 5),
+                            "false_accept_rate": round(counts[4 * j + 2] / max(1, counts[4 * j]), 5),
+                            "false_rejects": int(counts[4 * j + 3])} for j, e in enumerate(es)}}
+            del dist_
+        del steps_obj, reads, refs
+        torch.cuda.empty_cache()
+    clocks = sampler.stop()
+
+    ms_all = sharding.max_over_ranks(step_ms, device=dev)
+    keys = sorted(accepted)
+    acc_tot = dict(zip(keys, sharding.sum_over_ranks([accepted[k] for k in keys], device=dev)))
+    work = sum(n * len(es) for _, es, _, n in bk) if c5 else sum(
+        n * len(es) for _, es, _, n in bk) * world
+    value = work / (ms_all / 1e3) / 1e9
+
+    # roofline of every kernel family; the dominant one is the largest share of the step
+    ncu = load_ncu(f"{args.config}:{args.path}")
+    kernels = []
+    for kname, kms in kern_ms.items():
+        b, o, parts = kern_work[kname]
+        hbm = b / (kms / 1e3) / 1e9
+        alu = o / (kms / 1e3) / 1e12
+        bound = "alu" if alu / alu_peak > hbm / hbm_peak else "hbm"
+        ent = {"kernel": kname, "bound": bound,
+               "achieved": round(alu if bound == "alu" else hbm, 3),
+               "peak": round(alu_peak if bound == "alu" else hbm_peak, 3),
+               "unit": "T int-ops/s" if bound == "alu" else "GB/s",
+               "frac": round((alu / alu_peak) if bound == "alu" else (hbm / hbm_peak), 4),
+               "hbm_frac": round(hbm / hbm_peak, 4), "alu_frac": round(alu / alu_peak, 4),
+               "share_of_step": round(kms / step_ms, 4), "ms_per_step": round(kms, 4),
+               "algorithmic_bytes_per_step": b, "algorithmic_ops_per_step": o,
+               "per_launch_group": parts,
+               "peak_source": alu_src if bound == "alu" else peak_src}
+        if ncu:
+            hit = [v for k, v in ncu.items() if kname in k]
+            if hit:
+                ent["traffic"] = hit[0].get("traffic_bytes_per_launch")
+                if "pipe_alu_pct" in hit[0]:
+                    ent["ncu_pipe_alu_pct"] = hit[0]["pipe_alu_pct"]
+        ent.setdefault("traffic", None)
+        kernels.append(ent)
+    roof = dict(max(kernels, key=lambda k: k["share_of_step"]))
+    roof["all_kernels"] = [{k: v for k, v in x.items() if k in (
+        "kernel", "bound", "frac", "hbm_frac", "alu_frac", "achieved", "unit", "share_of_step",
+        "traffic")} for x in kernels]
+
+    e2e = None if args.no_e2e else measure_e2e(args, ctx, bk)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, args.cpu_budget)
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": unit_of(args), "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_all, 4),
+        "higher_is_better": True, "scaling": "strong" if c5 else "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic", "config": config_of(args, world),
+        "pairs_per_s": round(sum(n for *_, n in bk) * (1 if c5 else world) / (ms_all / 1e3) / 1e9, 4),
+        "roofline": roof, "per_bucket": per_bucket, "accepted": acc_tot,
+        "int_peak_T_ops_s": ip, "gpu_launches": launches, "clocks": clocks, "e2e": e2e,
+        "cpu_baseline": cpu, "paper": PAPER[args.config], "accuracy": accuracy,
+        "timing": "CUDA events on the launching stream around K steps after W warm-ups, per "
+                  "resident chunk; step time = sum over the rank's chunks; max over ranks",
+    }
+    if c5:
+        line["chunks_rank0"] = len(plan)
+    return line
 
 
-def measure_e2e(gk, torch, dev, n, L, es, rank, world, args):
-    """Same metric through the public host-buffer API (gk_filter_host_sweep): every
-    step copies the batch host->device once and the results of every e device->host."""
+def measure_e2e(args, ctx, bk):
+    """The same metric through the public host-buffer C-ABI calls: every step copies a
+    sample of each bucket's pairs host->device (pinned) and the results device->host.
+    c5: gk_filter_host (fused filtration per chunk, 2-stream pipeline); c2-c4:
+    gk_filter_host_sweep.  Time per pair per bucket x the bucket's share = the step."""
     import pairgen
-    n_e2e = n
-    # host copies of this rank's shard (pinned)
-    r_h, f_h = pairgen.gen_pairs_cuda(n_e2e, L, idx0=rank * n, device=dev)
-    hr = torch.empty((n_e2e, L), dtype=torch.uint8, pin_memory=True)
-    hf = torch.empty((n_e2e, L), dtype=torch.uint8, pin_memory=True)
-    hr.copy_(r_h)
-    hf.copy_(f_h)
-    del r_h, f_h
-    acc = torch.empty((len(es), gk.result_words(n_e2e)), dtype=torch.int32, pin_memory=True)
-    err = torch.empty((len(es), n_e2e), dtype=torch.uint8, pin_memory=True)
-    chunk = 1 << 21
-    ws = torch.empty(gk.host_sweep_workspace_bytes(chunk, L, L, max(es)), dtype=torch.uint8,
-                     device=dev)
-    torch.cuda.synchronize(dev)
+    torch, gk, sharding = ctx["torch"], ctx["gk"], ctx["sharding"]
+    world, rank, dev = ctx["world"], ctx["rank"], ctx["dev"]
+    c5 = args.config == "c5"
+    t_step, h2d, d2h, desc = 0.0, 0, 0, []
+    for L, es, idx0, n in bk:
+        lo, cnt = sharding.even_shard(n, rank, world) if c5 else sharding.weak_shard(n, rank)
+        ns = min(cnt, 1 << 23)
+        r_d, f_d = pairgen.gen_pairs_cuda(ns, L, idx0=idx0 + lo, device=dev)
+        hr = torch.empty((ns, L), dtype=torch.uint8, pin_memory=True)
+        hf = torch.empty((ns, L), dtype=torch.uint8, pin_memory=True)
+        hr.copy_(r_d)
+        hf.copy_(f_d)
+        del r_d, f_d
+        torch.cuda.empty_cache()
+        rows = len(es)
+        acc = torch.empty((rows, gk.result_words(ns)), dtype=torch.int32, pin_memory=True)
+        err = torch.empty((rows, ns), dtype=torch.uint8, pin_memory=True)
+        chunk = 1 << 21
+        if c5:
+            ws = torch.empty(gk.host_workspace_bytes(chunk, L), dtype=torch.uint8, device=dev)
 
-    def one():
-        gk.filter_host_sweep(hr, hf, es, L, accept=acc, errcount=err, workspace=ws,
-                             chunk_pairs=chunk)
+            def one():
+                gk.filter_host(hr, hf, es[0], L, accept=acc[0], errcount=err[0], workspace=ws,
+                               chunk_pairs=chunk)
+        else:
+            ws = torch.empty(gk.host_sweep_workspace_bytes(chunk, L, L, max(es)),
+                             dtype=torch.uint8, device=dev)
 
-    one()  # warm-up
-    steps = max(1, min(args.steps, 3))
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(steps):
+            def one():
+                gk.filter_host_sweep(hr, hf, list(es), L, accept=acc, errcount=err, workspace=ws,
+                                     chunk_pairs=chunk)
+        torch.cuda.synchronize(dev)
         one()
-    dt = (time.perf_counter() - t0) / steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([dt], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
-    value = n_e2e * len(es) * world / dt / 1e9
-    return {"value": round(value, 4), "unit": "Gpairs/s",
-            "h2d_GB_s": round(2 * n_e2e * L / dt / 1e9, 1),
-            "note": "bound by the host->device copy of the ASCII pairs (PCIe Gen5 x16, ~55-60 GB/s "
-                    "pinned); the device work of a step is ~4 ms of the ~110 ms",
-            "h2d_bytes_per_step": 2 * n_e2e * L,
-            "d2h_bytes_per_step": (n_e2e // 8 + n_e2e) * len(es),
-            "api": "gk_filter_host_sweep (pinned host buffers; each chunk copied + encoded once, "
-                   "filtered for every e in one gk_filter_sweep pass; 2-stream pipeline)",
-            "n_pairs_per_gpu": n_e2e, "timer": "host wall clock around the synchronous call"}
+        reps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            one()
+        dt = (time.perf_counter() - t0) / reps
+        t_step += dt * cnt / ns
+        h2d += 2 * ns * L
+        d2h += rows * (ns // 8 + ns)
+        desc.append(f"{ns} of {cnt} pairs at {L} bp")
+        del hr, hf, acc, err, ws
+        torch.cuda.empty_cache()
+    t_all = sharding.max_over_ranks(t_step, device=dev)
+    work = sum(n * len(es) for _, es, _, n in bk) * (1 if c5 else world)
+    return {"value": round(work / t_all / 1e9, 4), "unit": unit_of(args),
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": ("gk_filter_host (pinned host ASCII, fused filtration per 2M-pair chunk, 2 CUDA "
+                    "streams overlapping H2D / kernel / D2H)" if c5 else
+                    "gk_filter_host_sweep (pinned host ASCII; each chunk copied + encoded once, "
+                    "one gk_filter_sweep pass for every e)"),
+            "sample": "per bucket " + "; ".join(desc) + ": host wall clock around the synchronous "
+                      "call, time per pair x the rank's pairs; max over ranks",
+            "bound": "host->device copy of the ASCII pairs (PCIe)"}
 
 
 if __name__ == "__main__":

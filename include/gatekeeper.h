@@ -27,7 +27,8 @@
  *    GK_OK (0) or a negative gk_status.  A launch failure returns GK_ERR_CUDA;
  *    gk_last_cuda_error() then gives the cudaError_t (thread-local).
  *  - n = 0 is a valid no-op.  1 <= len <= GK_MAX_LEN; 0 <= e < len.
- *  - No global mutable state; calls from several host threads are safe.
+ *  - No global mutable state (apart from the diagnostic launch counter of
+ *    gk_launch_count, an atomic); calls from several host threads are safe.
  *
  * Packed sequence layout ("bit-sliced tiles", written by gk_encode, read by
  * gk_filter).  Sequences are grouped by 32 ("group") and groups by 32
@@ -80,6 +81,9 @@ int gk_version(void);
 const char* gk_status_string(int status);
 /* cudaError_t of the last GK_ERR_CUDA returned on this host thread (0 if none). */
 int gk_last_cuda_error(void);
+/* Number of CUDA kernels this process has launched through the library so far
+ * (process-wide atomic counter; the bench reads it around its timed region). */
+uint64_t gk_launch_count(void);
 
 /* Size queries (pure host functions, no CUDA). */
 size_t gk_packed_words(int64_t n_seqs, int32_t len); /* u32 words of a packed sequence set */

@@ -39,6 +39,7 @@ def _load():
         lib.gko_filter_pair.argtypes = [P, P, I, I, I, ctypes.POINTER(I), ctypes.POINTER(I), P]
         lib.gko_filter.argtypes = [P, P, I64, I, I64, I, I, P, P, I]
         lib.gko_sweep.argtypes = [P, P, I64, I, I64, I, I, P, P, I]
+        lib.gko_sweep_prefix.argtypes = [P, P, I64, I, I64, I, I, P, P, I]
         lib.gko_levenshtein.argtypes = [P, I, P, I]
         lib.gko_pack.argtypes = [P, I64, I, I64, P, P]
         lib.gko_xor_row.argtypes = [P, P, I, I, P]
@@ -47,6 +48,7 @@ def _load():
         lib.gko_count.argtypes = [P, I]
         lib.gko_edit_batch.argtypes = [P, P, I64, I, I64, P, I]
         for f in (lib.gko_code, lib.gko_filter_pair, lib.gko_filter, lib.gko_sweep,
+                  lib.gko_sweep_prefix,
                   lib.gko_levenshtein, lib.gko_pack, lib.gko_xor_row, lib.gko_count,
                   lib.gko_edit_batch):
             f.restype = ctypes.c_int
@@ -120,6 +122,24 @@ def sweep(reads: np.ndarray, refs: np.ndarray, emax: int, L: int | None = None,
                            int(edge_fix), acc.ctypes.data, err.ctypes.data, nthreads)
     if rc:
         raise ValueError(f"gko_sweep rejected arguments (rc={rc})")
+    return acc, err
+
+
+def sweep_prefix(reads: np.ndarray, refs: np.ndarray, emax: int, L: int | None = None,
+                 edge_fix: bool = True, nthreads: int | None = None):
+    """Same outputs as :func:`sweep` in one pass per pair: F_e = F_{e-1} & A*D_e & A*I_e
+    (gko_sweep_pair; pinned row for row against :func:`sweep`)."""
+    reads = np.ascontiguousarray(reads, dtype=np.uint8)
+    refs = np.ascontiguousarray(refs, dtype=np.uint8)
+    n, stride = reads.shape
+    L = stride if L is None else L
+    nthreads = (os.cpu_count() or 1) if nthreads is None else nthreads
+    acc = np.empty((emax + 1, n), dtype=np.uint8)
+    err = np.empty((emax + 1, n), dtype=np.uint8)
+    rc = _load().gko_sweep_prefix(reads.ctypes.data, refs.ctypes.data, n, L, stride, emax,
+                                  int(edge_fix), acc.ctypes.data, err.ctypes.data, nthreads)
+    if rc:
+        raise ValueError(f"gko_sweep_prefix rejected arguments (rc={rc})")
     return acc, err
 
 

@@ -174,6 +174,60 @@ int gko_filter_pair(const uint8_t* read, const uint8_t* ref, int L, int e, int e
   return 0;
 }
 
+/* Threshold sweep of one pair in a single pass (the prefix property of the AND
+ * chain): the final bit-vector for threshold e is
+ *     F_e = A0 AND (A*D_1 AND A*I_1) AND ... AND (A*D_e AND A*I_e)
+ * (PAPER.md:49 "2e+1 masks", :51 "AND"), so F_e = F_{e-1} AND A*D_e AND A*I_e
+ * and one pass over k = 1..emax yields F_e for every e <= emax.  Each k builds
+ * its masks exactly as gko_filter_pair does (same functions, same order).  The
+ * decision for each e is gko_filter_pair's: c0 <= e accepts with c0 (R5), e = 0
+ * rejects with c0 (:49), else count(F_e) decides (:51).  Pairs with c0 <= k
+ * need no F_k (every e >= c0 is decided by the Hamming stage), so the k loop
+ * stops there.  accept[e], err[e] for e = 0..emax (stride 1 per e). */
+int gko_sweep_pair(const uint8_t* read, const uint8_t* ref, int L, int emax, int edge_fix,
+                   uint8_t* accept, uint8_t* err, int64_t estride) {
+  int q[GKO_MAX_LEN], r[GKO_MAX_LEN];
+  uint8_t H0[GKO_MAX_LEN], A0[GKO_MAX_LEN], F[GKO_MAX_LEN];
+  uint8_t D[GKO_MAX_LEN], AD[GKO_MAX_LEN], I[GKO_MAX_LEN], AI[GKO_MAX_LEN];
+  if (L < 1 || L > GKO_MAX_LEN || emax < 0 || emax >= L) return -1;
+
+  int undefined = 0;
+  for (int i = 0; i < L; ++i) {
+    q[i] = gko_code(read[i]);
+    r[i] = gko_code(ref[i]);
+    if (q[i] < 0 || r[i] < 0) undefined = 1;
+  }
+  if (undefined) {                                     /* :95 */
+    for (int e = 0; e <= emax; ++e) { accept[e * estride] = 1; err[e * estride] = 255; }
+    return 0;
+  }
+  mask_from_xor(q, r, L, 0, H0);                       /* :49 */
+  gko_amend(H0, L, A0);                                /* :51 */
+  int c0 = gko_count(A0, L);
+  /* e = 0: no ASM (:49); every e >= c0: Hamming-stage accept (R5) */
+  accept[0] = c0 <= 0 ? 1 : 0;
+  err[0] = (uint8_t)c0;
+  for (int e = 1; e <= emax; ++e)
+    if (c0 <= e) { accept[e * estride] = 1; err[e * estride] = (uint8_t)c0; }
+
+  for (int i = 0; i < L; ++i) F[i] = A0[i];
+  for (int k = 1; k <= emax && k < c0; ++k) {          /* F_k = F_{k-1} & A*D_k & A*I_k */
+    mask_from_xor(q, r, L, +k, D);
+    mask_from_xor(q, r, L, -k, I);
+    gko_amend(D, L, AD);
+    gko_amend(I, L, AI);
+    if (edge_fix) {                                    /* :109 */
+      for (int i = 0; i < k && i < L; ++i) AD[i] = 1;
+      for (int i = L - k; i < L; ++i) if (i >= 0) AI[i] = 1;
+    }
+    for (int i = 0; i < L; ++i) F[i] = (uint8_t)(F[i] & AD[i] & AI[i]);
+    int c = gko_count(F, L);                           /* :51 decision for e = k */
+    accept[k * estride] = c <= k ? 1 : 0;
+    err[k * estride] = (uint8_t)c;
+  }
+  return 0;
+}
+
 /* ---- batch driver (pthreads; a pure scheduling wrapper) ------------------ */
 typedef struct {
   const uint8_t *reads, *refs;
@@ -194,6 +248,11 @@ static void* gko_worker(void* arg) {
       if (gko_filter_pair(rd, rf, j->L, j->e, j->edge_fix, &a, &c, 0)) { j->rc = -1; return 0; }
       j->accept[p] = (uint8_t)a;
       if (j->err) j->err[p] = (uint8_t)c;
+    } else if (j->sweep == 2) {
+      if (gko_sweep_pair(rd, rf, j->L, j->emax, j->edge_fix, j->accept + p, j->err + p, j->n)) {
+        j->rc = -1;
+        return 0;
+      }
     } else {
       for (int e = 0; e <= j->emax; ++e) {
         int a, c;
@@ -245,6 +304,20 @@ int gko_sweep(const uint8_t* reads, const uint8_t* refs, int64_t n, int L, int64
   memset(&j, 0, sizeof j);
   j.reads = reads; j.refs = refs; j.n = n; j.L = L; j.stride = stride; j.emax = emax;
   j.edge_fix = edge_fix; j.accept = accept; j.err = err; j.sweep = 1;
+  return gko_run(&j, nthreads);
+}
+
+/* Threshold sweep in one pass per pair (gko_sweep_pair): the same outputs as
+ * gko_sweep, pinned row for row against it (tests/test_oracle_sweep.py).
+ * Used for full-size parity, where e_max+1 independent filtrations per pair
+ * would cost hours of CPU. */
+int gko_sweep_prefix(const uint8_t* reads, const uint8_t* refs, int64_t n, int L, int64_t stride,
+                     int emax, int edge_fix, uint8_t* accept, uint8_t* err, int nthreads) {
+  if (n < 0 || L < 1 || L > GKO_MAX_LEN || stride < L || emax < 0 || emax >= L) return -1;
+  gko_job j;
+  memset(&j, 0, sizeof j);
+  j.reads = reads; j.refs = refs; j.n = n; j.L = L; j.stride = stride; j.emax = emax;
+  j.edge_fix = edge_fix; j.accept = accept; j.err = err; j.sweep = 2;
   return gko_run(&j, nthreads);
 }
 

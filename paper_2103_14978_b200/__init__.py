@@ -47,6 +47,7 @@ def load_library(path: str = LIB_PATH):
         "gk_version": (ctypes.c_int, []),
         "gk_status_string": (ctypes.c_char_p, [ctypes.c_int]),
         "gk_last_cuda_error": (ctypes.c_int, []),
+        "gk_launch_count": (ctypes.c_uint64, []),
         "gk_packed_words": (SZ, [I64, I32]),
         "gk_undef_words": (SZ, [I64]),
         "gk_result_words": (SZ, [I64]),
@@ -98,6 +99,11 @@ def _stream(stream=None):
 
 def _ptr(t):
     return None if t is None else t.data_ptr()
+
+
+def launch_count() -> int:
+    """Kernels launched through libgk.so by this process so far (gk_launch_count)."""
+    return int(load_library().gk_launch_count())
 
 
 # ---- size queries -------------------------------------------------------------

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/gatekeeper.h"
 #include "gk_kernels.cuh"
 
@@ -19,6 +21,11 @@ int launch_gather_windows(const uint32_t* planes, int64_t nbases, const int64_t*
 }  // namespace gk
 
 static thread_local int g_last_cuda_error = 0;
+static std::atomic<uint64_t> g_launches{0};
+
+namespace gk {
+void count_launch(int k) { g_launches.fetch_add((uint64_t)k, std::memory_order_relaxed); }
+}  // namespace gk
 
 static int cuda_status(cudaError_t err) {
   if (err == cudaSuccess) return GK_OK;
@@ -50,6 +57,8 @@ const char* gk_status_string(int status) {
 }
 
 int gk_last_cuda_error(void) { return g_last_cuda_error; }
+
+uint64_t gk_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 size_t gk_packed_words(int64_t n_seqs, int32_t len) {
   if (n_seqs <= 0 || len <= 0) return 0;

@@ -179,6 +179,7 @@ int launch_compact(const uint32_t* bits, int64_t n, uint32_t* idx, uint64_t* n_a
   const int64_t ctas = (nwords + CP_WORDS_PER_CTA - 1) / CP_WORDS_PER_CTA;
   uint32_t* counts = reinterpret_cast<uint32_t*>(ws);
   const dim3 grid((unsigned)ctas, (unsigned)rows);
+  count_launch(2);
   compact_count_kernel<<<grid, CP_THREADS, 0, stream>>>(bits, n, counts, bstride);
   compact_write_kernel<<<grid, CP_THREADS, 0, stream>>>(
       bits, n, counts, idx, reinterpret_cast<unsigned long long*>(n_acc), bstride, istride);

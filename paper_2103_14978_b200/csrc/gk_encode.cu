@@ -172,6 +172,7 @@ static void launch_tma(const uint8_t* seqs, int64_t nblocks, int len, int stride
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > nblocks) grid = nblocks;
+  count_launch();
   kern<<<(unsigned)grid, 128, smem, stream>>>(seqs, nblocks, len, stride, packed, undef);
 }
 
@@ -208,6 +209,7 @@ static void launch_generic(const uint8_t* seqs, int64_t n, int len, int64_t stri
     cudaFuncSetAttribute(encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   }
+  count_launch();
   if (aligned)
     encode_kernel<true><<<(unsigned)blocks, gpc * 32, smem, stream>>>(seqs, n, len, stride,
                                                                       packed, undef, gpc, first_group);
@@ -223,7 +225,10 @@ int launch_encode(const uint8_t* seqs, int64_t n, int len, int64_t stride, uint3
   const bool tma_ok = ((reinterpret_cast<uintptr_t>(seqs) & 15u) == 0) && stride <= 512 &&
                       GK_ENCODE_TMA;
   if (tma_ok) {
-    const int64_t nblocks = n / 128;  // full blocks of 4 groups
+    // full blocks of 4 groups; a block copies 128*stride bytes, so when stride > len
+    // the block holding the last row would read stride-len bytes past the caller's
+    // (n-1)*stride+len: that block goes to the generic path, which stops at len
+    const int64_t nblocks = stride == len ? n / 128 : (n - 1) / 128;
     if (nblocks > 0) {
       if (stride <= 128) dispatch_tma<128>(seqs, nblocks, len, (int)stride, packed, undef, stream);
       else if (stride <= 256) dispatch_tma<256>(seqs, nblocks, len, (int)stride, packed, undef, stream);
@@ -237,6 +242,7 @@ int launch_encode(const uint8_t* seqs, int64_t n, int len, int64_t stride, uint3
     const int64_t total = (tile_end - ngroups) * len;
     const int threads = 256;
     const int64_t tb = (total + threads - 1) / threads;
+    count_launch();
     encode_tail_kernel<<<(unsigned)(tb < 1024 ? tb : 1024), threads, 0, stream>>>(
         ngroups, tile_end, len, packed, undef);
   }

@@ -104,6 +104,7 @@ static void launch_sp(const uint2* reads, const uint2* refs, const uint32_t* run
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(filter_sp_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+  count_launch();
   filter_sp_kernel<E><<<(unsigned)blocks, warps * 32, smem, stream>>>(reads, refs, rund, fund, n,
                                                                        len, accept, errc);
 }
@@ -151,6 +152,7 @@ int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* r
     cudaFuncSetAttribute(filter_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   const int64_t blocks = (tiles + warps - 1) / warps;
+  count_launch();
   filter_generic_kernel<<<(unsigned)blocks, warps * 32, smem, stream>>>(r2, f2, rund, fund, n,
                                                                         len, e, accept, errc,
                                                                         edge_fix);

@@ -302,6 +302,7 @@ static void launch_ascii_tma(const uint8_t* reads, const uint8_t* refs, int stri
   auto kern = filter_ascii_tma_kernel<E, PMAX>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  count_launch();
   kern<<<(unsigned)ntiles, 128, smem, stream>>>(reads, refs, stride, ntiles, n, len, e, accept,
                                                 errc);
 }
@@ -314,7 +315,9 @@ static int64_t try_ascii_tma(const uint8_t* reads, const uint8_t* refs, int64_t 
   if (!GK_ASCII_TMA) return 0;
   if (((reinterpret_cast<uintptr_t>(reads) | reinterpret_cast<uintptr_t>(refs)) & 15u) != 0)
     return 0;
-  const int64_t ntiles = n / 1024;
+  // a tile copies 1024*stride bytes per set: with stride > len the tile holding the
+  // last row would over-read the caller's (n-1)*stride+len bytes -> generic path
+  const int64_t ntiles = stride == len ? n / 1024 : (n - 1) / 1024;
   if (ntiles == 0) return 0;
   // the generic fallback (E < 0) keeps F[len][32] in the staging area
   if (E < 0 && (size_t)len * 32 * 4 > (size_t)4 * 2 * 32 * (stride <= 128 ? 128 : stride <= 256 ? 256 : 512))
@@ -335,6 +338,7 @@ static void launch_ascii_t(const uint8_t* reads, const uint8_t* refs, int64_t st
   if (L.total > 48 * 1024)
     cudaFuncSetAttribute(filter_ascii_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)L.total);
+  count_launch();
   filter_ascii_kernel<E><<<(unsigned)blocks, 128, L.total, stream>>>(
       reads, refs, stride, n, len, e, L.G, (uint32_t)L.packed, (uint32_t)L.staging, accept, errc);
 }

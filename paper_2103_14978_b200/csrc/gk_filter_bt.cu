@@ -422,6 +422,7 @@ void launch_bt(const uint2* reads, const uint2* refs, const uint32_t* rund, cons
   const int64_t blocks = (tiles + warps - 1) / warps;
   // no shared memory: give the whole unified L1 to the read windows' reuse
   cudaFuncSetAttribute(filter_bt_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+  count_launch();
   filter_bt_kernel<<<(unsigned)blocks, warps * 32, 0, stream>>>(reads, refs, rund, fund, n, len, e,
                                                                  accept, errc, edge_fix);
 }
@@ -495,6 +496,7 @@ static void launch_sweep_np(const uint2* reads, const uint2* refs, const uint32_
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(filter_bt_sweep_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+  count_launch();
   filter_bt_sweep_kernel<NP><<<(unsigned)blocks, SWEEP_WARPS * 32, smem, stream>>>(
       reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix);
 }

@@ -15,6 +15,7 @@
 // bit-sliced packed layout of gk_encode (include/gatekeeper.h), which
 // gk_filter / gk_filter_sweep consume unchanged.
 #include "gk_common.cuh"
+#include "gk_kernels.cuh"
 
 namespace gk {
 
@@ -129,6 +130,7 @@ int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int len, int64_t str
   const int64_t nwords = (total + 31) / 32 + 1;  // + 1: the funnel shift's look-ahead word
   int64_t blocks = (nwords + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  count_launch();
   pack_planes_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rows, n_rows, len, stride,
                                                            reinterpret_cast<uint4*>(planes), nwords);
   return 0;
@@ -137,6 +139,7 @@ int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int len, int64_t str
 int launch_gather_windows(const uint32_t* planes, int64_t nbases, const int64_t* offsets, int64_t n,
                           int len, uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
   const int64_t tiles = (n + 1023) / 1024;  // whole tiles (zero-filled tail)
+  count_launch();
   gather_windows_kernel<<<(unsigned)tiles, 1024, 0, stream>>>(
       reinterpret_cast<const uint4*>(planes), nbases, offsets, n, len, packed, undef);
   return 0;

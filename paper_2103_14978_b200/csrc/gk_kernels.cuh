@@ -9,6 +9,10 @@
 
 namespace gk {
 
+// Process-wide count of kernels launched by the library (gk_launch_count in the
+// C ABI): the bench's "gpu_launches" is read from it, not estimated.
+void count_launch(int k = 1);
+
 int launch_encode(const uint8_t* seqs, int64_t n, int len, int64_t stride, uint32_t* packed,
                   uint32_t* undef, cudaStream_t stream);
 

@@ -110,6 +110,7 @@ static void launch_ed(const uint8_t* reads, const uint8_t* refs, int64_t stride,
     cudaFuncSetAttribute(edit_distance_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   const int64_t blocks = (n + ED_THREADS - 1) / ED_THREADS;
+  count_launch();
   edit_distance_kernel<W><<<(unsigned)blocks, ED_THREADS, smem, stream>>>(reads, refs, stride, n,
                                                                            len, dist);
 }
@@ -170,6 +171,7 @@ int launch_accuracy(const uint32_t* accept, int64_t astride, const uint8_t* errc
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t blocks = (n + 255) / 256;
   if (blocks > 4 * sms) blocks = 4 * sms;
+  count_launch();
   accuracy_kernel<<<dim3((unsigned)blocks, (unsigned)rows), 256, 0, stream>>>(
       accept, astride, errc, estride, dist, n, e_list, counts);
   return 0;

@@ -18,3 +18,16 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden_dir():
     return GOLDEN
+
+
+@pytest.fixture(scope="session")
+def gk():
+    """The product library, built in-tree (nvcc) and loaded; needs a CUDA device."""
+    import torch
+
+    import paper_2103_14978_b200 as m
+    from paper_2103_14978_b200 import _build
+    _build.build()
+    m.load_library()
+    assert torch.cuda.is_available(), "GPU test without a CUDA device"
+    return m
