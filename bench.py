@@ -77,7 +77,7 @@ def parse(argv=None):
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c5", choices=["c2", "c3", "c4", "c5"])
     p.add_argument("--path", default=None,
-                   help="c5: fused (default) | packed;  c2-c4: sweep (default) | packed | fused")
+                   help="c5: packed (default) | fused;  c2-c4: sweep (default) | packed | fused")
     p.add_argument("--total", type=int, default=None, help="c5: total pairs (default 1B)")
     p.add_argument("--n", type=int, default=None, help="c2-c4: pairs per GPU (default 30M)")
     p.add_argument("--mem-gb", type=float, default=110.0,
@@ -91,7 +91,7 @@ def parse(argv=None):
                    help="seconds of host work for the oracle baseline")
     a = p.parse_args(argv)
     if a.path is None:
-        a.path = "fused" if a.config == "c5" else "sweep"
+        a.path = "packed" if a.config == "c5" else "sweep"
     return a
 
 
@@ -617,7 +617,8 @@ def run_buckets(args, ctx):
 def measure_e2e(args, ctx, bk):
     """The same metric through the public host-buffer C-ABI calls: every step copies a
     sample of each bucket's pairs host->device (pinned) and the results device->host.
-    c5: gk_filter_host (fused filtration per chunk, 2-stream pipeline); c2-c4:
+    c5: gk_filter_host (encode + filter + compaction per chunk, 2-stream pipeline; the
+    accepted indices come back); c2-c4:
     gk_filter_host_sweep.  Time per pair per bucket x the bucket's share = the step."""
     import pairgen
     torch, gk, sharding = ctx["torch"], ctx["gk"], ctx["sharding"]
@@ -639,11 +640,12 @@ def measure_e2e(args, ctx, bk):
         err = torch.empty((rows, ns), dtype=torch.uint8, pin_memory=True)
         chunk = 1 << 21
         if c5:
-            ws = torch.empty(gk.host_workspace_bytes(chunk, L), dtype=torch.uint8, device=dev)
+            ws = torch.empty(gk.host_workspace_bytes(chunk, L, L), dtype=torch.uint8, device=dev)
+            idx = torch.empty(ns, dtype=torch.uint32, pin_memory=True)
 
             def one():
-                gk.filter_host(hr, hf, es[0], L, accept=acc[0], errcount=err[0], workspace=ws,
-                               chunk_pairs=chunk)
+                gk.filter_host(hr, hf, es[0], L, want_accept=False, indices=True, idx=idx,
+                               workspace=ws, chunk_pairs=chunk)
         else:
             ws = torch.empty(gk.host_sweep_workspace_bytes(chunk, L, L, max(es)),
                              dtype=torch.uint8, device=dev)
@@ -660,16 +662,24 @@ def measure_e2e(args, ctx, bk):
         dt = (time.perf_counter() - t0) / reps
         t_step += dt * cnt / ns
         h2d += 2 * ns * L
-        d2h += rows * (ns // 8 + ns)
+        if c5:
+            _, _, got = gk.filter_host(hr, hf, es[0], L, want_accept=False, indices=True, idx=idx,
+                                       workspace=ws, chunk_pairs=chunk)
+            d2h += 4 * got.numel() + 8 * ((ns + chunk - 1) // chunk)
+        else:
+            d2h += rows * (ns // 8 + ns)
         desc.append(f"{ns} of {cnt} pairs at {L} bp")
         del hr, hf, acc, err, ws
+        if c5:
+            del idx
         torch.cuda.empty_cache()
     t_all = sharding.max_over_ranks(t_step, device=dev)
     work = sum(n * len(es) for _, es, _, n in bk) * (1 if c5 else world)
     return {"value": round(work / t_all / 1e9, 4), "unit": unit_of(args),
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "api": ("gk_filter_host (pinned host ASCII, fused filtration per 2M-pair chunk, 2 CUDA "
-                    "streams overlapping H2D / kernel / D2H)" if c5 else
+            "api": ("gk_filter_host (pinned host ASCII; per 2M-pair chunk gk_encode x2 + gk_filter "
+                    "+ gk_compact, only the accepted pairs' indices come back; 2 CUDA streams "
+                    "overlapping H2D / kernels / D2H)" if c5 else
                     "gk_filter_host_sweep (pinned host ASCII; each chunk copied + encoded once, "
                     "one gk_filter_sweep pass for every e)"),
             "sample": "per bucket " + "; ".join(desc) + ": host wall clock around the synchronous "

@@ -226,13 +226,16 @@ int gk_gather_windows(const uint32_t* d_planes, int64_t n_bases, const int64_t* 
  *  h_errcount    : (e_max+1) rows of n_pairs bytes (host, written) or NULL.
  *  d_ws          : gk_host_index_workspace_bytes(chunk_pairs, len, e_max) bytes,
  *                  256-byte aligned; chunk_pairs a multiple of 1024.
+ *  stream        : the call is ordered after all work already enqueued on it (e.g.
+ *                  the gk_pack_planes that produced the planes); see gk_filter_host.
  * Synchronous.  Errors: as gk_gather_windows + GK_ERR_E, GK_ERR_WORKSPACE. */
 size_t gk_host_index_workspace_bytes(int64_t chunk_pairs, int32_t len, int32_t e_max);
 int gk_filter_host_index(const uint32_t* d_read_planes, int64_t read_bases,
                          const uint32_t* d_ref_planes, int64_t ref_bases,
                          const int64_t* h_read_offsets, const int64_t* h_ref_offsets,
                          int64_t n_pairs, int32_t len, int32_t e_max, uint32_t* h_accept_bits,
-                         uint8_t* h_errcount, void* d_ws, size_t ws_bytes, int64_t chunk_pairs);
+                         uint8_t* h_errcount, void* d_ws, size_t ws_bytes, int64_t chunk_pairs,
+                         void* stream);
 
 /* Accuracy harness: the ground truth of the paper's
  * accuracy study -- exact global edit distance, as Edlib in global mode
@@ -258,22 +261,34 @@ int gk_accuracy(const uint32_t* d_accept_bits, int64_t bits_row_stride, const ui
                 int64_t err_row_stride, const int32_t* d_dist, int64_t n_pairs,
                 const int32_t* d_e_list, int32_t n_rows, uint64_t* d_counts, void* stream);
 
-/* End-to-end from HOST buffers (the paper's "filter time"): streams
- * the pairs through device memory in chunks, overlapping host->device copies,
- * filtering and device->host copies on two CUDA streams.
+/* End-to-end from HOST buffers (the paper's "filter time"): the
+ * pairs stream through device memory in chunks on two CUDA streams, overlapping
+ * the host->device copy of one chunk with the kernels of the next and the
+ * device->host copy of the previous one.  Per chunk: gk_encode of both sets,
+ * gk_filter at threshold e and, if indices are requested, gk_compact (the
+ * accepted pairs handed on to verification).
  *  h_reads, h_refs : n_pairs rows of `stride` bytes in host memory (pinned memory
  *                    gives full PCIe / C2C bandwidth; pageable works).
- *  h_accept_bits   : gk_result_words(n_pairs) u32 in host memory (written).
+ *  h_accept_bits   : gk_result_words(n_pairs) u32 in host memory (written) or NULL.
  *  h_errcount      : n_pairs bytes in host memory (written) or NULL.
- *  d_ws            : device scratch of gk_host_workspace_bytes(chunk_pairs, stride) bytes;
- *                    chunk_pairs (a multiple of 1024, > 0) sets the pipeline granularity.
+ *  h_idx, h_n_acc  : ascending indices of the accepted pairs (room for n_pairs
+ *                    u32; n_pairs < 2^32) and their number (one u64), or both
+ *                    NULL.  At least one of h_accept_bits / h_idx is required.
+ *  d_ws            : device scratch of gk_host_workspace_bytes(chunk_pairs, stride,
+ *                    len) bytes, 256-byte aligned; chunk_pairs (a multiple of 1024,
+ *                    > 0) sets the pipeline granularity.
+ *  stream          : the call is ordered after all work already enqueued on it
+ *                    (e.g. the producer of d_ws); the pipeline runs on two
+ *                    internal streams (created once per host thread and device,
+ *                    with a 16-byte pinned count buffer, and reused).
  * Synchronous: returns after the results are in host memory.
  * Errors: as gk_filter_ascii + GK_ERR_WORKSPACE. */
-size_t gk_host_workspace_bytes(int64_t chunk_pairs, int64_t stride);
+size_t gk_host_workspace_bytes(int64_t chunk_pairs, int64_t stride, int32_t len);
 int gk_filter_host(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride,
                    int64_t n_pairs, int32_t len, int32_t e,
                    uint32_t* h_accept_bits, uint8_t* h_errcount,
-                   void* d_ws, size_t ws_bytes, int64_t chunk_pairs);
+                   uint32_t* h_idx, uint64_t* h_n_acc,
+                   void* d_ws, size_t ws_bytes, int64_t chunk_pairs, void* stream);
 
 /* Threshold sweep from HOST buffers: every chunk of pairs crosses PCIe and is
  * encoded once, then filtered for every e <= e_max = max(e_list) in one pass
@@ -284,12 +299,13 @@ int gk_filter_host(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride
  *  h_errcount      : n_e * n_pairs bytes, row t = e_list[t] (written) or NULL.
  *  d_ws            : gk_host_sweep_workspace_bytes(chunk_pairs, stride, len, e_max)
  *                    bytes (e_max = the largest threshold of e_list).
+ *  stream          : as gk_filter_host.
  * Synchronous.  Errors: as gk_filter_host. */
 size_t gk_host_sweep_workspace_bytes(int64_t chunk_pairs, int64_t stride, int32_t len, int32_t e_max);
 int gk_filter_host_sweep(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride,
                          int64_t n_pairs, int32_t len, const int32_t* e_list, int32_t n_e,
                          uint32_t* h_accept_bits, uint8_t* h_errcount,
-                         void* d_ws, size_t ws_bytes, int64_t chunk_pairs);
+                         void* d_ws, size_t ws_bytes, int64_t chunk_pairs, void* stream);
 
 #ifdef __cplusplus
 }

@@ -63,15 +63,15 @@ def load_library(path: str = LIB_PATH):
         "gk_plane_words": (SZ, [I64]),
         "gk_host_index_workspace_bytes": (SZ, [I64, I32, I32]),
         "gk_filter_host_index": (ctypes.c_int, [P, I64, P, I64, P, P, I64, I32, I32, P, P, P, SZ,
-                                                I64]),
+                                                I64, P]),
         "gk_pack_planes": (ctypes.c_int, [P, I64, I32, I64, P, P]),
         "gk_gather_windows": (ctypes.c_int, [P, I64, P, I64, I32, P, P, P]),
         "gk_accuracy": (ctypes.c_int, [P, I64, P, I64, P, I64, P, I32, P, P]),
         "gk_compact_rows": (ctypes.c_int, [P, I32, I64, I64, P, I64, P, P, SZ, P]),
-        "gk_host_workspace_bytes": (SZ, [I64, I64]),
-        "gk_filter_host": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P, SZ, I64]),
+        "gk_host_workspace_bytes": (SZ, [I64, I64, I32]),
+        "gk_filter_host": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P, P, P, SZ, I64, P]),
         "gk_host_sweep_workspace_bytes": (SZ, [I64, I64, I32, I32]),
-        "gk_filter_host_sweep": (ctypes.c_int, [P, P, I64, I64, I32, P, I32, P, P, P, SZ, I64]),
+        "gk_filter_host_sweep": (ctypes.c_int, [P, P, I64, I64, I32, P, I32, P, P, P, SZ, I64, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -268,7 +268,7 @@ def gather_windows(planes, n_bases: int, offsets, length: int, out=None, stream=
 
 def filter_host_index(read_planes, read_bases: int, ref_planes, ref_bases: int, read_offsets,
                       ref_offsets, length: int, e_max: int, accept=None, errcount=None,
-                      workspace=None, chunk_pairs: int = 1 << 21):
+                      workspace=None, chunk_pairs: int = 1 << 21, stream=None):
     """Index mode from HOST int64 offset tensors (planes on the device) -> host result
     rows (accept bits [e_max+1, words], errcount [e_max+1, n] or None)."""
     import torch
@@ -285,7 +285,7 @@ def filter_host_index(read_planes, read_bases: int, ref_planes, ref_bases: int, 
                                                read_offsets.data_ptr(), ref_offsets.data_ptr(), n,
                                                length, e_max, accept.data_ptr(), _ptr(errcount),
                                                workspace.data_ptr(), workspace.numel(),
-                                               chunk_pairs), "gk_filter_host_index")
+                                               chunk_pairs, _stream(stream)), "gk_filter_host_index")
     return accept, errcount
 
 
@@ -317,26 +317,37 @@ def accuracy(accept, errcount, dist, n: int, e_list, stream=None):
 
 
 # ---- end to end from host buffers ----------------------------------------------
-def host_workspace_bytes(chunk_pairs: int, stride: int) -> int:
-    return load_library().gk_host_workspace_bytes(chunk_pairs, stride)
+def host_workspace_bytes(chunk_pairs: int, stride: int, length: int | None = None) -> int:
+    return load_library().gk_host_workspace_bytes(chunk_pairs, stride,
+                                                  stride if length is None else length)
 
 
 def filter_host(reads, refs, e: int, length: int | None = None, accept=None, errcount=None,
-                workspace=None, chunk_pairs: int = 1 << 20):
-    """End-to-end filtration of HOST (CPU, ideally pinned) uint8 tensors; results in host memory."""
+                indices: bool = False, idx=None, workspace=None, chunk_pairs: int = 1 << 20,
+                want_accept: bool = True, stream=None):
+    """End-to-end filtration of HOST (CPU, ideally pinned) uint8 tensors; results in host
+    memory -> (accept bits or None, errcount or None, accepted indices or None).  With
+    indices=True the chunks are compacted on the device and only the ascending indices of
+    the accepted pairs come back (a uint32 tensor of length n_acc)."""
     import torch
     n, stride = reads.shape
     length = stride if length is None else length
-    if accept is None:
+    if accept is None and want_accept:
         accept = torch.empty(max(1, result_words(n)), dtype=torch.int32, pin_memory=True)
+    if indices and idx is None:
+        idx = torch.empty(max(1, n), dtype=torch.uint32, pin_memory=True)
+    n_acc = ctypes.c_uint64(0)
     if workspace is None:
-        workspace = torch.empty(host_workspace_bytes(chunk_pairs, stride), dtype=torch.uint8,
-                                device="cuda")
+        workspace = torch.empty(host_workspace_bytes(chunk_pairs, stride, length),
+                                dtype=torch.uint8, device="cuda")
     _check(load_library().gk_filter_host(reads.data_ptr(), refs.data_ptr(), stride, n, length, e,
-                                         accept.data_ptr(), _ptr(errcount),
-                                         workspace.data_ptr(), workspace.numel(), chunk_pairs),
+                                         _ptr(accept), _ptr(errcount),
+                                         _ptr(idx) if indices else None,
+                                         ctypes.byref(n_acc) if indices else None,
+                                         workspace.data_ptr(), workspace.numel(), chunk_pairs,
+                                         _stream(stream)),
            "gk_filter_host")
-    return accept, errcount
+    return accept, errcount, (idx[:n_acc.value] if indices else None)
 
 
 def host_sweep_workspace_bytes(chunk_pairs: int, stride: int, length: int, e_max: int) -> int:
@@ -344,7 +355,7 @@ def host_sweep_workspace_bytes(chunk_pairs: int, stride: int, length: int, e_max
 
 
 def filter_host_sweep(reads, refs, e_list, length: int | None = None, accept=None,
-                      errcount=None, workspace=None, chunk_pairs: int = 1 << 20):
+                      errcount=None, workspace=None, chunk_pairs: int = 1 << 20, stream=None):
     """Threshold sweep of HOST uint8 tensors: each chunk is copied and encoded once, then
     filtered for every e <= max(e_list) in one pass.  Returns (accept bits [n_e, words], errcount [n_e, n] or None)."""
     import torch
@@ -361,6 +372,6 @@ def filter_host_sweep(reads, refs, e_list, length: int | None = None, accept=Non
     _check(load_library().gk_filter_host_sweep(reads.data_ptr(), refs.data_ptr(), stride, n,
                                                length, es, len(e_list), accept.data_ptr(),
                                                _ptr(errcount), workspace.data_ptr(),
-                                               workspace.numel(), chunk_pairs),
+                                               workspace.numel(), chunk_pairs, _stream(stream)),
            "gk_filter_host_sweep")
     return accept, errcount

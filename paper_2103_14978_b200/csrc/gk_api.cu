@@ -258,105 +258,214 @@ int gk_accuracy(const uint32_t* d_accept_bits, int64_t bits_row_stride, const ui
   return after_launch();
 }
 
-// ---- host-buffer end-to-end pipeline ------------------------------------------
+// ---- host-buffer end-to-end pipelines -----------------------------------------
+// Chunks of pairs stream through two buffer sets on two CUDA streams, so the
+// host->device copy of chunk c+1 overlaps the kernels of chunk c and the
+// device->host copy of chunk c-1 (the paper's "filter time").
+// The streams, events and a small pinned count buffer are created once per
+// (host thread, device) and reused across calls.  Every call is ordered after
+// the work already enqueued on the caller's `stream` (its internal streams wait
+// on an event recorded there) and returns once the results are in host memory.
 static size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-size_t gk_host_workspace_bytes(int64_t chunk_pairs, int64_t stride) {
-  if (chunk_pairs <= 0 || stride <= 0) return 0;
-  const size_t in = round_up((size_t)chunk_pairs * (size_t)stride, 256);
-  const size_t acc = round_up((size_t)(chunk_pairs / 32 + 1) * 4, 256);
-  const size_t err = round_up((size_t)chunk_pairs, 256);
-  return 2 * (2 * in + acc + err);
+namespace {
+struct HostRes {
+  bool ready = false;
+  cudaStream_t st[2];
+  cudaEvent_t ev_in, ev_cnt[2];
+  unsigned long long* cnt = nullptr;  // pinned, 2 counts
+};
+constexpr int kMaxDev = 64;
+thread_local HostRes g_host[kMaxDev];
+
+int host_begin(void* stream, HostRes** out) {
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return cuda_status(err);
+  if (dev < 0 || dev >= kMaxDev) return GK_ERR_ARG;
+  HostRes& r = g_host[dev];
+  if (!r.ready) {
+    for (int b = 0; b < 2; ++b) {
+      if ((err = cudaStreamCreateWithFlags(&r.st[b], cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_status(err);
+      if ((err = cudaEventCreateWithFlags(&r.ev_cnt[b], cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_status(err);
+    }
+    if ((err = cudaEventCreateWithFlags(&r.ev_in, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_status(err);
+    if ((err = cudaHostAlloc(reinterpret_cast<void**>(&r.cnt), 2 * sizeof(unsigned long long),
+                             cudaHostAllocDefault)) != cudaSuccess)
+      return cuda_status(err);
+    r.ready = true;
+  }
+  // order both pipeline streams after the caller's stream (its producers of
+  // device inputs / workspace)
+  if ((err = cudaEventRecord(r.ev_in, (cudaStream_t)stream)) != cudaSuccess) return cuda_status(err);
+  for (int b = 0; b < 2; ++b)
+    if ((err = cudaStreamWaitEvent(r.st[b], r.ev_in, 0)) != cudaSuccess) return cuda_status(err);
+  *out = &r;
+  return GK_OK;
 }
 
-int gk_filter_host(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride,
-                   int64_t n_pairs, int32_t len, int32_t e, uint32_t* h_accept_bits,
-                   uint8_t* h_errcount, void* d_ws, size_t ws_bytes, int64_t chunk_pairs) {
-  int rc = check_ascii(h_reads, n_pairs, len, stride);
-  if (rc) return rc;
-  if (e < 0 || e >= len) return GK_ERR_E;
-  if (n_pairs == 0) return GK_OK;
-  if (!h_refs || !h_accept_bits) return GK_ERR_ARG;
-  if (chunk_pairs <= 0 || chunk_pairs % 1024 != 0) return GK_ERR_ARG;
-  if (!d_ws || ws_bytes < gk_host_workspace_bytes(chunk_pairs, stride)) return GK_ERR_WORKSPACE;
-  if (!aligned(d_ws, 256)) return GK_ERR_ALIGN;
-
-  const size_t in = round_up((size_t)chunk_pairs * (size_t)stride, 256);
-  const size_t acc = round_up((size_t)(chunk_pairs / 32 + 1) * 4, 256);
-  const size_t errb = round_up((size_t)chunk_pairs, 256);
-  uint8_t* base = static_cast<uint8_t*>(d_ws);
-  struct Buf { uint8_t *r, *f; uint32_t* a; uint8_t* c; } buf[2];
+int host_end(HostRes* r, int rc) {
   for (int b = 0; b < 2; ++b) {
-    uint8_t* p = base + b * (2 * in + acc + errb);
-    buf[b].r = p;
-    buf[b].f = p + in;
-    buf[b].a = reinterpret_cast<uint32_t*>(p + 2 * in);
-    buf[b].c = p + 2 * in + acc;
-  }
-  cudaStream_t st[2];
-  for (int b = 0; b < 2; ++b) {
-    cudaError_t err = cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking);
-    if (err != cudaSuccess) {
-      if (b == 1) cudaStreamDestroy(st[0]);
-      return cuda_status(err);
-    }
-  }
-  rc = GK_OK;
-  const int64_t nchunks = (n_pairs + chunk_pairs - 1) / chunk_pairs;
-  for (int64_t c = 0; c < nchunks && rc == GK_OK; ++c) {
-    const int b = (int)(c & 1);
-    const int64_t p0 = c * chunk_pairs;
-    const int64_t np = (n_pairs - p0) < chunk_pairs ? (n_pairs - p0) : chunk_pairs;
-    const size_t bytes = (size_t)((np - 1) * stride + len);
-    cudaError_t err = cudaMemcpyAsync(buf[b].r, h_reads + p0 * stride, bytes,
-                                      cudaMemcpyHostToDevice, st[b]);
-    if (err == cudaSuccess)
-      err = cudaMemcpyAsync(buf[b].f, h_refs + p0 * stride, bytes, cudaMemcpyHostToDevice, st[b]);
-    if (err != cudaSuccess) { rc = cuda_status(err); break; }
-    gk::launch_filter_ascii(buf[b].r, buf[b].f, stride, np, len, e, buf[b].a,
-                            h_errcount ? buf[b].c : nullptr, st[b]);
-    rc = after_launch();
-    if (rc) break;
-    err = cudaMemcpyAsync(h_accept_bits + p0 / 32, buf[b].a, (size_t)((np + 31) / 32) * 4,
-                          cudaMemcpyDeviceToHost, st[b]);
-    if (err == cudaSuccess && h_errcount)
-      err = cudaMemcpyAsync(h_errcount + p0, buf[b].c, (size_t)np, cudaMemcpyDeviceToHost, st[b]);
-    if (err != cudaSuccess) { rc = cuda_status(err); break; }
-  }
-  for (int b = 0; b < 2; ++b) {
-    cudaError_t err = cudaStreamSynchronize(st[b]);
+    cudaError_t err = cudaStreamSynchronize(r->st[b]);
     if (rc == GK_OK && err != cudaSuccess) rc = cuda_status(err);
-    cudaStreamDestroy(st[b]);
   }
   return rc;
 }
 
-// ---- host-buffer threshold sweep ---------------------------------------------
-struct SweepLayout {
-  size_t in, packed, undef, acc, err, per_set;
+// Index lists of a chunked pipeline: chunk c's accepted indices (absolute, written
+// by the compaction kernel with base p0) are copied back once its count is known
+// -- the host waits for chunk c-1's count while chunk c runs.
+struct IdxDrain {
+  HostRes* r;
+  uint32_t* h_idx;
+  unsigned long long total = 0;
+  int pending = -1;         // buffer set of the chunk waiting to be drained
+  const uint32_t* d_idx[2];
+  int drain() {
+    if (pending < 0) return GK_OK;
+    const int b = pending;
+    pending = -1;
+    cudaError_t err = cudaEventSynchronize(r->ev_cnt[b]);
+    if (err != cudaSuccess) return cuda_status(err);
+    const unsigned long long n = r->cnt[b];
+    if (n) {
+      err = cudaMemcpyAsync(h_idx + total, d_idx[b], (size_t)n * 4, cudaMemcpyDeviceToHost,
+                            r->st[b]);
+      if (err != cudaSuccess) return cuda_status(err);
+    }
+    total += n;
+    return GK_OK;
+  }
+};
+}  // namespace
+
+struct HostLayout {
+  size_t in, packed, undef, acc, err, idx, nacc, cws, per_set;
 };
 
-static SweepLayout sweep_layout(int64_t chunk, int64_t stride, int32_t len, int32_t e_max) {
-  SweepLayout L;
+static HostLayout host_layout(int64_t chunk, int64_t stride, int32_t len, int32_t rows) {
+  HostLayout L;
   L.in = round_up((size_t)chunk * (size_t)stride, 256);
   L.packed = round_up(gk_packed_words(chunk, len) * 4, 256);
   L.undef = round_up(gk_undef_words(chunk) * 4, 256);
   L.acc = round_up((size_t)(chunk / 32) * 4, 256);  // chunk is a multiple of 1024
   L.err = round_up((size_t)chunk, 256);
-  L.per_set = 2 * L.in + 2 * L.packed + 2 * L.undef + (size_t)(e_max + 1) * (L.acc + L.err);
+  L.idx = round_up((size_t)chunk * 4, 256);
+  L.nacc = 256;
+  L.cws = round_up(gk::compact_workspace_bytes(chunk), 256);
+  L.per_set = 2 * L.in + 2 * L.packed + 2 * L.undef + (size_t)rows * (L.acc + L.err) + L.idx +
+              L.nacc + L.cws;
   return L;
 }
 
+struct SetPtrs {
+  uint8_t *r, *f;
+  uint32_t *pq, *pr, *uq, *ur, *acc;
+  uint8_t* err;
+  uint32_t* idx;
+  uint64_t* nacc;
+  void* cws;
+};
+
+static SetPtrs set_ptrs(void* ws, const HostLayout& L, int b, int rows) {
+  uint8_t* p = static_cast<uint8_t*>(ws) + (size_t)b * L.per_set;
+  SetPtrs s;
+  s.r = p; p += L.in;
+  s.f = p; p += L.in;
+  s.pq = reinterpret_cast<uint32_t*>(p); p += L.packed;
+  s.pr = reinterpret_cast<uint32_t*>(p); p += L.packed;
+  s.uq = reinterpret_cast<uint32_t*>(p); p += L.undef;
+  s.ur = reinterpret_cast<uint32_t*>(p); p += L.undef;
+  s.acc = reinterpret_cast<uint32_t*>(p); p += (size_t)rows * L.acc;
+  s.err = p; p += (size_t)rows * L.err;
+  s.idx = reinterpret_cast<uint32_t*>(p); p += L.idx;
+  s.nacc = reinterpret_cast<uint64_t*>(p); p += L.nacc;
+  s.cws = p;
+  return s;
+}
+
+size_t gk_host_workspace_bytes(int64_t chunk_pairs, int64_t stride, int32_t len) {
+  if (chunk_pairs <= 0 || stride <= 0 || len <= 0) return 0;
+  return 2 * host_layout(chunk_pairs, stride, len, 1).per_set;
+}
+
+int gk_filter_host(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride,
+                   int64_t n_pairs, int32_t len, int32_t e, uint32_t* h_accept_bits,
+                   uint8_t* h_errcount, uint32_t* h_idx, uint64_t* h_n_acc, void* d_ws,
+                   size_t ws_bytes, int64_t chunk_pairs, void* stream) {
+  int rc = check_ascii(h_reads, n_pairs, len, stride);
+  if (rc) return rc;
+  if (e < 0 || e >= len) return GK_ERR_E;
+  if (h_idx && !h_n_acc) return GK_ERR_ARG;
+  if (h_idx && n_pairs >= ((int64_t)1 << 32)) return GK_ERR_ARG;
+  if (n_pairs == 0) {
+    if (h_n_acc) *h_n_acc = 0;
+    return GK_OK;
+  }
+  if (!h_refs || (!h_accept_bits && !h_idx)) return GK_ERR_ARG;
+  if (chunk_pairs <= 0 || chunk_pairs % 1024 != 0) return GK_ERR_ARG;
+  if (!d_ws || ws_bytes < gk_host_workspace_bytes(chunk_pairs, stride, len))
+    return GK_ERR_WORKSPACE;
+  if (!aligned(d_ws, 256)) return GK_ERR_ALIGN;
+  const HostLayout L = host_layout(chunk_pairs, stride, len, 1);
+  HostRes* res = nullptr;
+  if ((rc = host_begin(stream, &res)) != GK_OK) return rc;
+  IdxDrain drain{res, h_idx};
+  const int64_t nchunks = (n_pairs + chunk_pairs - 1) / chunk_pairs;
+  for (int64_t c = 0; c < nchunks && rc == GK_OK; ++c) {
+    const int b = (int)(c & 1);
+    cudaStream_t st = res->st[b];
+    const SetPtrs s = set_ptrs(d_ws, L, b, 1);
+    drain.d_idx[b] = s.idx;
+    const int64_t p0 = c * chunk_pairs;
+    const int64_t np = (n_pairs - p0) < chunk_pairs ? (n_pairs - p0) : chunk_pairs;
+    const size_t bytes = (size_t)((np - 1) * stride + len);
+    cudaError_t err = cudaMemcpyAsync(s.r, h_reads + p0 * stride, bytes, cudaMemcpyHostToDevice, st);
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(s.f, h_refs + p0 * stride, bytes, cudaMemcpyHostToDevice, st);
+    if (err != cudaSuccess) { rc = cuda_status(err); break; }
+    // a1 twice, a2-a6 (the same kernels as gk_encode + gk_filter), a7 if asked
+    gk::launch_encode(s.r, np, len, stride, s.pq, s.uq, st);
+    gk::launch_encode(s.f, np, len, stride, s.pr, s.ur, st);
+    gk::launch_filter(s.pq, s.pr, s.uq, s.ur, np, len, e, s.acc, h_errcount ? s.err : nullptr, 0, st);
+    if (h_idx)
+      gk::launch_compact(s.acc, np, s.idx, s.nacc, s.cws, st, 1, 0, 0, (uint32_t)p0);
+    if ((rc = after_launch()) != GK_OK) break;
+    if (h_accept_bits)
+      err = cudaMemcpyAsync(h_accept_bits + p0 / 32, s.acc, (size_t)((np + 31) / 32) * 4,
+                            cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess && h_errcount)
+      err = cudaMemcpyAsync(h_errcount + p0, s.err, (size_t)np, cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess && h_idx) {
+      err = cudaMemcpyAsync(&res->cnt[b], s.nacc, 8, cudaMemcpyDeviceToHost, st);
+      if (err == cudaSuccess) err = cudaEventRecord(res->ev_cnt[b], st);
+    }
+    if (err != cudaSuccess) { rc = cuda_status(err); break; }
+    if (h_idx) {
+      if ((rc = drain.drain()) != GK_OK) break;  // chunk c-1, while chunk c runs
+      drain.pending = b;
+    }
+  }
+  if (rc == GK_OK && h_idx) rc = drain.drain();
+  rc = host_end(res, rc);
+  if (rc == GK_OK && h_n_acc) *h_n_acc = drain.total;
+  return rc;
+}
+
+// ---- host-buffer threshold sweep ---------------------------------------------
 size_t gk_host_sweep_workspace_bytes(int64_t chunk_pairs, int64_t stride, int32_t len,
                                      int32_t e_max) {
   if (chunk_pairs <= 0 || stride <= 0 || len <= 0 || e_max < 0) return 0;
-  return 2 * sweep_layout(chunk_pairs, stride, len, e_max).per_set;
+  return 2 * host_layout(chunk_pairs, stride, len, e_max + 1).per_set;
 }
 
 int gk_filter_host_sweep(const uint8_t* h_reads, const uint8_t* h_refs, int64_t stride,
                          int64_t n_pairs, int32_t len, const int32_t* e_list, int32_t n_e,
                          uint32_t* h_accept_bits, uint8_t* h_errcount, void* d_ws,
-                         size_t ws_bytes, int64_t chunk_pairs) {
+                         size_t ws_bytes, int64_t chunk_pairs, void* stream) {
   int rc = check_ascii(h_reads, n_pairs, len, stride);
   if (rc) return rc;
   if (n_e <= 0 || !e_list) return GK_ERR_ARG;
@@ -370,61 +479,41 @@ int gk_filter_host_sweep(const uint8_t* h_reads, const uint8_t* h_refs, int64_t 
   if (!d_ws || ws_bytes < gk_host_sweep_workspace_bytes(chunk_pairs, stride, len, e_max))
     return GK_ERR_WORKSPACE;
   if (!aligned(d_ws, 256)) return GK_ERR_ALIGN;
-  const SweepLayout L = sweep_layout(chunk_pairs, stride, len, e_max);
+  const HostLayout L = host_layout(chunk_pairs, stride, len, e_max + 1);
   const size_t words_total = gk_result_words(n_pairs);
-  cudaStream_t st[2];
-  for (int b = 0; b < 2; ++b) {
-    cudaError_t err = cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking);
-    if (err != cudaSuccess) {
-      if (b == 1) cudaStreamDestroy(st[0]);
-      return cuda_status(err);
-    }
-  }
-  rc = GK_OK;
+  HostRes* res = nullptr;
+  if ((rc = host_begin(stream, &res)) != GK_OK) return rc;
   const int64_t nchunks = (n_pairs + chunk_pairs - 1) / chunk_pairs;
   for (int64_t c = 0; c < nchunks && rc == GK_OK; ++c) {
     const int b = (int)(c & 1);
-    uint8_t* base = static_cast<uint8_t*>(d_ws) + b * L.per_set;
-    uint8_t* dr = base;
-    uint8_t* df = dr + L.in;
-    uint32_t* pq = reinterpret_cast<uint32_t*>(df + L.in);
-    uint32_t* pr = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(pq) + L.packed);
-    uint32_t* uq = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(pr) + L.packed);
-    uint32_t* ur = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(uq) + L.undef);
-    uint8_t* outs = reinterpret_cast<uint8_t*>(ur) + L.undef;
+    cudaStream_t st = res->st[b];
+    const SetPtrs s = set_ptrs(d_ws, L, b, e_max + 1);
     const int64_t p0 = c * chunk_pairs;
     const int64_t np = (n_pairs - p0) < chunk_pairs ? (n_pairs - p0) : chunk_pairs;
     const size_t bytes = (size_t)((np - 1) * stride + len);
-    cudaError_t err = cudaMemcpyAsync(dr, h_reads + p0 * stride, bytes, cudaMemcpyHostToDevice,
-                                      st[b]);
+    cudaError_t err = cudaMemcpyAsync(s.r, h_reads + p0 * stride, bytes, cudaMemcpyHostToDevice, st);
     if (err == cudaSuccess)
-      err = cudaMemcpyAsync(df, h_refs + p0 * stride, bytes, cudaMemcpyHostToDevice, st[b]);
+      err = cudaMemcpyAsync(s.f, h_refs + p0 * stride, bytes, cudaMemcpyHostToDevice, st);
     if (err != cudaSuccess) { rc = cuda_status(err); break; }
-    gk::launch_encode(dr, np, len, stride, pq, uq, st[b]);
-    gk::launch_encode(df, np, len, stride, pr, ur, st[b]);
-    // every e <= e_max in one pass (gk_filter_sweep); rows of the chunk: [e][chunk/32] bits,
-    // then [e][chunk] counts
-    uint32_t* acc = reinterpret_cast<uint32_t*>(outs);
-    uint8_t* ec = h_errcount ? outs + (size_t)(e_max + 1) * L.acc : nullptr;
-    gk::launch_filter_sweep(pq, pr, uq, ur, np, len, e_max, acc, ec, 0, st[b]);
+    gk::launch_encode(s.r, np, len, stride, s.pq, s.uq, st);
+    gk::launch_encode(s.f, np, len, stride, s.pr, s.ur, st);
+    // every e <= e_max in one pass (gk_filter_sweep); rows of the chunk: [e][np/32]
+    // bits, then [e][np] counts
+    uint8_t* ec = h_errcount ? s.err : nullptr;
+    gk::launch_filter_sweep(s.pq, s.pr, s.uq, s.ur, np, len, e_max, s.acc, ec, 0, st);
     rc = after_launch();
     const size_t words = (size_t)((np + 31) / 32);
     for (int t = 0; t < n_e && rc == GK_OK; ++t) {
       const int e = e_list[t];
       err = cudaMemcpyAsync(h_accept_bits + (size_t)t * words_total + p0 / 32,
-                            acc + (size_t)e * words, words * 4, cudaMemcpyDeviceToHost, st[b]);
+                            s.acc + (size_t)e * words, words * 4, cudaMemcpyDeviceToHost, st);
       if (err == cudaSuccess && h_errcount)
-        err = cudaMemcpyAsync(h_errcount + (size_t)t * n_pairs + p0, ec + (size_t)e * np,
-                              (size_t)np, cudaMemcpyDeviceToHost, st[b]);
+        err = cudaMemcpyAsync(h_errcount + (size_t)t * n_pairs + p0, s.err + (size_t)e * np,
+                              (size_t)np, cudaMemcpyDeviceToHost, st);
       if (err != cudaSuccess) rc = cuda_status(err);
     }
   }
-  for (int b = 0; b < 2; ++b) {
-    cudaError_t err = cudaStreamSynchronize(st[b]);
-    if (rc == GK_OK && err != cudaSuccess) rc = cuda_status(err);
-    cudaStreamDestroy(st[b]);
-  }
-  return rc;
+  return host_end(res, rc);
 }
 
 // ---- host-buffer index mode ----------------------------------------------------
@@ -446,7 +535,8 @@ int gk_filter_host_index(const uint32_t* d_read_planes, int64_t read_bases,
                          const uint32_t* d_ref_planes, int64_t ref_bases,
                          const int64_t* h_read_offsets, const int64_t* h_ref_offsets,
                          int64_t n_pairs, int32_t len, int32_t e_max, uint32_t* h_accept_bits,
-                         uint8_t* h_errcount, void* d_ws, size_t ws_bytes, int64_t chunk_pairs) {
+                         uint8_t* h_errcount, void* d_ws, size_t ws_bytes, int64_t chunk_pairs,
+                         void* stream) {
   if (n_pairs < 0 || read_bases < 0 || ref_bases < 0) return GK_ERR_ARG;
   if (len < 1 || len > GK_MAX_LEN) return GK_ERR_LEN;
   if (e_max < 0 || e_max >= len) return GK_ERR_E;
@@ -460,18 +550,14 @@ int gk_filter_host_index(const uint32_t* d_read_planes, int64_t read_bases,
     return GK_ERR_ALIGN;
   const size_t per_set = index_chunk_bytes(chunk_pairs, len, e_max);
   const size_t words_total = gk_result_words(n_pairs);
-  cudaStream_t st[2];
-  for (int b = 0; b < 2; ++b) {
-    cudaError_t err = cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking);
-    if (err != cudaSuccess) {
-      if (b == 1) cudaStreamDestroy(st[0]);
-      return cuda_status(err);
-    }
-  }
-  int rc = GK_OK;
+  const size_t acc_row = round_up((size_t)(chunk_pairs / 32) * 4, 256);
+  HostRes* res = nullptr;
+  int rc = host_begin(stream, &res);
+  if (rc != GK_OK) return rc;
   const int64_t nchunks = (n_pairs + chunk_pairs - 1) / chunk_pairs;
   for (int64_t c = 0; c < nchunks && rc == GK_OK; ++c) {
     const int b = (int)(c & 1);
+    cudaStream_t st = res->st[b];
     uint8_t* base = static_cast<uint8_t*>(d_ws) + b * per_set;
     int64_t* d_roff = reinterpret_cast<int64_t*>(base);
     int64_t* d_foff = d_roff + chunk_pairs;
@@ -486,34 +572,27 @@ int gk_filter_host_index(const uint32_t* d_read_planes, int64_t read_bases,
     const int64_t p0 = c * chunk_pairs;
     const int64_t np = (n_pairs - p0) < chunk_pairs ? (n_pairs - p0) : chunk_pairs;
     cudaError_t err = cudaMemcpyAsync(d_roff, h_read_offsets + p0, (size_t)np * 8,
-                                      cudaMemcpyHostToDevice, st[b]);
+                                      cudaMemcpyHostToDevice, st);
     if (err == cudaSuccess)
-      err = cudaMemcpyAsync(d_foff, h_ref_offsets + p0, (size_t)np * 8, cudaMemcpyHostToDevice,
-                            st[b]);
+      err = cudaMemcpyAsync(d_foff, h_ref_offsets + p0, (size_t)np * 8, cudaMemcpyHostToDevice, st);
     if (err != cudaSuccess) { rc = cuda_status(err); break; }
-    gk::launch_gather_windows(d_read_planes, read_bases, d_roff, np, len, pq, uq, st[b]);
-    gk::launch_gather_windows(d_ref_planes, ref_bases, d_foff, np, len, pr, ur, st[b]);
+    gk::launch_gather_windows(d_read_planes, read_bases, d_roff, np, len, pq, uq, st);
+    gk::launch_gather_windows(d_ref_planes, ref_bases, d_foff, np, len, pr, ur, st);
     const size_t words = (size_t)((np + 31) / 32);
     uint32_t* acc = reinterpret_cast<uint32_t*>(outs);
-    uint8_t* ec = h_errcount ? outs + (size_t)(e_max + 1) * round_up((size_t)(chunk_pairs / 32) * 4, 256)
-                             : nullptr;
-    gk::launch_filter_sweep(pq, pr, uq, ur, np, len, e_max, acc, ec, 0, st[b]);
+    uint8_t* ec = h_errcount ? outs + (size_t)(e_max + 1) * acc_row : nullptr;
+    gk::launch_filter_sweep(pq, pr, uq, ur, np, len, e_max, acc, ec, 0, st);
     rc = after_launch();
     for (int e = 0; e <= e_max && rc == GK_OK; ++e) {
       err = cudaMemcpyAsync(h_accept_bits + (size_t)e * words_total + p0 / 32, acc + (size_t)e * words,
-                            words * 4, cudaMemcpyDeviceToHost, st[b]);
+                            words * 4, cudaMemcpyDeviceToHost, st);
       if (err == cudaSuccess && h_errcount)
         err = cudaMemcpyAsync(h_errcount + (size_t)e * n_pairs + p0, ec + (size_t)e * np, (size_t)np,
-                              cudaMemcpyDeviceToHost, st[b]);
+                              cudaMemcpyDeviceToHost, st);
       if (err != cudaSuccess) rc = cuda_status(err);
     }
   }
-  for (int b = 0; b < 2; ++b) {
-    cudaError_t err = cudaStreamSynchronize(st[b]);
-    if (rc == GK_OK && err != cudaSuccess) rc = cuda_status(err);
-    cudaStreamDestroy(st[b]);
-  }
-  return rc;
+  return host_end(res, rc);
 }
 
 }  // extern "C"

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(CP_THREADS) compact_count_kernel(const uint32_
 __global__ void __launch_bounds__(CP_THREADS) compact_write_kernel(
     const uint32_t* __restrict__ bits, int64_t n, const uint32_t* __restrict__ cta_counts,
     uint32_t* __restrict__ idx, unsigned long long* __restrict__ n_acc, int64_t bstride,
-    int64_t istride) {
+    int64_t istride, uint32_t ibase) {
   bits += blockIdx.y * bstride;
   cta_counts += (size_t)blockIdx.y * gridDim.x;
   if (idx != nullptr) idx += blockIdx.y * istride;
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(CP_THREADS) compact_write_kernel(
       }
       const uint32_t tot = __shfl_sync(0xFFFFFFFFu, x, 31);
       uint32_t pos = x - c;
-      const uint32_t base = (uint32_t)((wbase + 32 * t + lane) * 32);
+      const uint32_t base = (uint32_t)((wbase + 32 * t + lane) * 32) + ibase;
       while (w) {
         st[pos++] = base + (uint32_t)(__ffs(w) - 1);
         w &= w - 1u;
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(CP_THREADS) compact_write_kernel(
         const uint32_t v = __shfl_sync(0xFFFFFFFFu, words[t], src);
         if (v == 0u) continue;
         if ((v >> lane) & 1u)
-          idx[o + __popc(v & lt)] = (uint32_t)((wbase + 32 * t + src) * 32 + lane);
+          idx[o + __popc(v & lt)] = (uint32_t)((wbase + 32 * t + src) * 32 + lane) + ibase;
         o += __popc(v);
       }
     }
@@ -174,7 +174,8 @@ size_t compact_workspace_bytes(int64_t n, int rows) {
 
 // rows x ceil(n/65536) CTAs per kernel: one launch pair for a whole batch of rows
 int launch_compact(const uint32_t* bits, int64_t n, uint32_t* idx, uint64_t* n_acc, void* ws,
-                   cudaStream_t stream, int rows, int64_t bstride, int64_t istride) {
+                   cudaStream_t stream, int rows, int64_t bstride, int64_t istride,
+                   uint32_t ibase) {
   const int64_t nwords = (n + 31) / 32;
   const int64_t ctas = (nwords + CP_WORDS_PER_CTA - 1) / CP_WORDS_PER_CTA;
   uint32_t* counts = reinterpret_cast<uint32_t*>(ws);
@@ -182,7 +183,7 @@ int launch_compact(const uint32_t* bits, int64_t n, uint32_t* idx, uint64_t* n_a
   count_launch(2);
   compact_count_kernel<<<grid, CP_THREADS, 0, stream>>>(bits, n, counts, bstride);
   compact_write_kernel<<<grid, CP_THREADS, 0, stream>>>(
-      bits, n, counts, idx, reinterpret_cast<unsigned long long*>(n_acc), bstride, istride);
+      bits, n, counts, idx, reinterpret_cast<unsigned long long*>(n_acc), bstride, istride, ibase);
   return 0;
 }
 

@@ -7,17 +7,13 @@
 // writes the bit-sliced layout of include/gatekeeper.h, in which a 32-bit word
 // holds one base position of 32 sequences.
 //
-// Per 4 bytes the work is branch-free SWAR integer code:
-//   * validity: m = ((w & 0x26) | 0x41) + 15*[bit2 & ~bit1] per byte reproduces
-//     the byte iff it is one of A C G T a c g t (the 8 values m can take are
-//     exactly that set), so bad |= w ^ m is 0 iff all 4 bytes are valid;
-//   * code planes: plane0 (high) = ASCII bit 2, plane1 (low) = bit 1 ^ bit 2
-//     (A 0x41 -> 00, C 0x43 -> 01, G 0x47 -> 10, T 0x54 -> 11, case-free);
-//   * transposition: a 4x4 byte transpose (8 PRMT) turns 4 rows x 4 positions
-//     into 4 positions x 4 rows, then one IMAD per plane gathers bit b of the 4
-//     bytes into a nibble (no carries: see gather_bit2/gather_bit1) and one funnel
-//     shift appends the nibble to the 32-sequence word.
+// The full blocks of 128 sequences run encode3_kernel (gk_encode3.cuh: per 4
+// bytes a SWAR validity test + code-bit extraction, then a 3-stage shuffle
+// transpose per 16 positions; about 1.6 ALU + 1.25 FMA instructions per input
+// byte); the rest (a partial last block, misaligned input) runs the generic
+// encode_kernel (gk_encode_core.cuh, 4x4 byte transposes + bit gathers).
 #include "gk_common.cuh"
+#include "gk_encode3.cuh"
 #include "gk_encode_core.cuh"
 #include "gk_kernels.cuh"
 #include "gk_tma.cuh"
@@ -25,18 +21,6 @@
 #ifndef GK_ENCODE_TMA
 #define GK_ENCODE_TMA 1
 #endif
-// minimum resident CTAs per SM requested from ptxas for the TMA encoder (A/B knob)
-#ifndef GK_ENC_MINB
-#define GK_ENC_MINB 1
-#endif
-// The 256-byte staging variant runs at 3 CTAs per SM (168 registers) when its last
-// lane-iteration is the sparse shared-quad tail (len <= 192, e.g. 150 bp: 1.63 ->
-// 1.54 ms per 30M) and at the register-unbounded 2 CTAs per SM otherwise (250 bp:
-// 3 CTAs measured 2.11 -> 2.19 ms); profiles/r01l_encoder_wide_minb_ab.jsonl.
-#ifndef GK_ENC_MINB_SPARSE
-#define GK_ENC_MINB_SPARSE 3
-#endif
-
 namespace gk {
 
 // Generic encoder: any alignment / stride / tail; also the tail of the TMA path.
@@ -88,24 +72,62 @@ __global__ void encode_tail_kernel(int64_t first_group, int64_t end_group, int l
   }
 }
 
-// TMA encoder: full blocks of 4 groups (128 sequences).  Persistent CTAs of 4
-// warps; warp w encodes group 4b+w of block b.  Its 32 rows (one contiguous span
-// of 32*stride bytes) arrive by one cp.async.bulk into a double buffer, the next
-// block's span being prefetched while the current one is encoded.  The 4 groups'
-// words are collected in shared memory and written out as full 32-byte sectors.
-template <int PMAX, int SM4, bool LPART, int MB>
-__global__ void __launch_bounds__(128, MB) encode_tma_kernel(const uint8_t* __restrict__ seqs,
+// TMA encoder (gk_encode3.cuh): full blocks of 4 groups (128 sequences).
+// Persistent CTAs of 4 warps; warp w encodes group 4b+w of block b.  Its 32
+// rows (one contiguous span of 32*stride bytes) arrive by one cp.async.bulk into
+// a per-warp double buffer, the next block's span being prefetched while the
+// current one is encoded.  The 4 groups' words are collected in shared memory
+// ([plane][position*5 + group]: conflict-free transposed writes; one buffer, so
+// that 3 CTAs fit an SM at 250 bp) and leave as full 32-byte sectors (4 groups x
+// 8 bytes per position).
+// NCH > 0: compile-time number of 16-position chunks (immediate LDS offsets);
+// NCH == 0: runtime.  ALN: every row start is 4-byte aligned (stride % 4 == 0).
+template <bool ALN>
+__device__ __forceinline__ void enc3_chunk(const uint8_t* buf, const uint32_t (&roff)[4],
+                                           const uint32_t (&rsh)[4], int c, int len,
+                                           const enc3::Lane& ln, uint32_t (&ag)[4],
+                                           uint32_t (&ay)[4], uint32_t* outs, uint32_t P,
+                                           int wg, bool tail) {
+  uint32_t x[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint8_t* a = buf + roff[i] + 16 * c;
+    uint32_t w;
+    if (ALN) {
+      w = *reinterpret_cast<const uint32_t*>(a);
+    } else {
+      const uint32_t lo = *reinterpret_cast<const uint32_t*>(a);
+      const uint32_t hi = *reinterpret_cast<const uint32_t*>(a + 4);
+      w = __funnelshift_r(lo, hi, rsh[i]);
+    }
+    if (tail) {  // bytes of positions >= len read as 'A' (valid, never stored)
+      const int rem = len - 16 * c - 4 * ln.cw;
+      const uint32_t bm =
+          rem >= 4 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * rem)));
+      w = (w & bm) | (0x41414141u & ~bm);
+    }
+    x[i] = enc3::row_word(w, ln, ag[i], ay[i]);
+  }
+  uint32_t m = enc3::merge4(x[0], x[1], x[2], x[3], ln);
+  m = enc3::transpose3(m, ln);
+  // lane = cw + 4b' + 8k: position 16c + 4cw + k, plane b' (0 = low -> paper plane 1)
+  const int lane = threadIdx.x & 31;
+  const int pos = 16 * c + 4 * (lane & 3) + (lane >> 3);
+  const int plane = ((lane >> 2) & 1) ? 0 : 1;
+  if (!tail || pos < len) outs[plane * P + pos * 5 + wg] = m;
+}
+
+template <int NCH, bool ALN, int MB>
+__global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restrict__ seqs,
                                                          int64_t nblocks, int len, int stride,
+                                                         uint32_t bufb, uint32_t P,
                                                          uint32_t* __restrict__ packed,
                                                          uint32_t* __restrict__ undef) {
-  constexpr int NIT = PMAX / 128;          // quad iterations per lane (4 bytes x 32 lanes)
-  constexpr uint32_t BUF = 32u * PMAX;     // bytes of one staging buffer
   extern __shared__ __align__(128) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* stage = sm + (size_t)warp * 2 * BUF;                    // [2][32*PMAX]
-  const int nq = (len + 3) >> 2;
-  uint2* outt0 = reinterpret_cast<uint2*>(sm + 4 * 2 * BUF);       // 2 x [4 warps][4 m][nq]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 4 * 2 * BUF + (size_t)2 * 16 * 8 * nq);
+  uint8_t* stage = sm + (size_t)warp * 2 * bufb;                               // [2][bufb]
+  uint32_t* outs = reinterpret_cast<uint32_t*>(sm + (size_t)4 * 2 * bufb);     // [2][P]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(outs + 2 * P);
   uint64_t* mybar = bars + 2 * warp;
   if (lane == 0) {
     mbar_init(&mybar[0], 1);
@@ -113,9 +135,17 @@ __global__ void __launch_bounds__(128, MB) encode_tma_kernel(const uint8_t* __re
     fence_mbar_init();
   }
   __syncwarp();
-  RowAddr<SM4> ra;
-  ra.init(smem_u32(stage), (uint32_t)stride, lane);
+  enc3::Lane ln;
+  ln.init(lane);
+  uint32_t roff[4], rsh[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t a = (uint32_t)ln.rows[i] * (uint32_t)stride + 4u * (uint32_t)ln.cw;
+    roff[i] = ALN ? a : (a & ~3u);
+    rsh[i] = (a & 3u) * 8u;
+  }
   const uint32_t span = 32u * (uint32_t)stride;
+  const int nch = NCH > 0 ? NCH : (len + 15) >> 4;
 
   int64_t b = blockIdx.x;
   if (b >= nblocks) return;
@@ -123,24 +153,33 @@ __global__ void __launch_bounds__(128, MB) encode_tma_kernel(const uint8_t* __re
     mbar_arrive_expect_tx(&mybar[0], span);
     tma_load_1d(stage, seqs + (4 * b + warp) * (int64_t)span, span, &mybar[0]);
   }
-  for (int i = 0; b < nblocks; ++i, b += gridDim.x) {
-    const int buf = i & 1;
+  for (int it = 0; b < nblocks; ++it, b += gridDim.x) {
+    const int buf = it & 1;
     const int64_t bn = b + gridDim.x;
     if (lane == 0 && bn < nblocks) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&mybar[buf ^ 1], span);
-      tma_load_1d(stage + (buf ^ 1) * BUF, seqs + (4 * bn + warp) * (int64_t)span, span,
+      tma_load_1d(stage + (buf ^ 1) * bufb, seqs + (4 * bn + warp) * (int64_t)span, span,
                   &mybar[buf ^ 1]);
     }
-    mbar_wait(&mybar[buf], (uint32_t)(i >> 1) & 1u);  // buffer buf's (i>>1)-th use
-    const int64_t g = 4 * b + warp;
-    uint2* outt = outt0 + (size_t)(i & 1) * 16 * nq;  // double-buffered: one barrier per block
-    uint2* myout = outt + (size_t)warp * 4 * nq;
-    auto emit = [&](int q, int m, uint32_t hi, uint32_t lo) { myout[m * nq + q] = make_uint2(hi, lo); };
-    const uint32_t und = buf == 0 ? encode_group_v2<SM4, LPART, NIT, 0u>(ra, len, emit)
-                                  : encode_group_v2<SM4, LPART, NIT, BUF>(ra, len, emit);
-    if (lane == 0) undef[g] = und;
-    __syncwarp();
+    mbar_wait(&mybar[buf], (uint32_t)(it >> 1) & 1u);
+    const uint8_t* sbuf = stage + buf * bufb;
+    // one output staging buffer (smem for more CTAs per SM): the previous block's
+    // copy-out must be complete before it is overwritten
+    if (it > 0) __syncthreads();
+    uint32_t ag[4] = {0u, 0u, 0u, 0u}, ay[4] = {0u, 0u, 0u, 0u};
+    if (NCH > 0) {
+#pragma unroll
+      for (int c = 0; c < (NCH > 1 ? NCH - 1 : 0); ++c)
+        enc3_chunk<ALN>(sbuf, roff, rsh, c, len, ln, ag, ay, outs, P, warp, false);
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < nch - 1; ++c)
+        enc3_chunk<ALN>(sbuf, roff, rsh, c, len, ln, ag, ay, outs, P, warp, false);
+    }
+    enc3_chunk<ALN>(sbuf, roff, rsh, nch - 1, len, ln, ag, ay, outs, P, warp, true);
+    const uint32_t und = enc3::group_undef(ag, ay, ln);
+    if (lane == 0) undef[4 * b + warp] = und;
     __syncthreads();
     // write the 4 groups' words: per position 32 contiguous bytes
     const int64_t tile = (4 * b) >> 5;
@@ -148,48 +187,71 @@ __global__ void __launch_bounds__(128, MB) encode_tma_kernel(const uint8_t* __re
     uint2* dst = reinterpret_cast<uint2*>(packed);
     for (int t = threadIdx.x; t < 4 * len; t += 128) {
       const int pos = t >> 2, w = t & 3;
-      dst[((tile * len + pos) * 32 + gl0 + w)] = outt[((size_t)w * 4 + (pos & 3)) * nq + (pos >> 2)];
+      dst[((tile * len + pos) * 32 + gl0 + w)] =
+          make_uint2(outs[pos * 5 + w], outs[P + pos * 5 + w]);
     }
   }
 }
 
-template <int PMAX, int SM4, bool LPART>
-static void launch_tma(const uint8_t* seqs, int64_t nblocks, int len, int stride,
-                       uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
-  const int nq = (len + 3) >> 2;
-  const size_t smem = (size_t)4 * 2 * 32 * PMAX + (size_t)2 * 16 * 8 * nq + 64;
-  constexpr int MB = PMAX == 128 ? GK_ENC_MINB : 1;
-  constexpr int MB_SPARSE = PMAX == 256 ? GK_ENC_MINB_SPARSE : MB;
-  const bool sparse_tail = PMAX == 256 && nq - 32 <= 16;  // NIT = 2, R <= 16 quads
-  auto kern = sparse_tail ? encode_tma_kernel<PMAX, SM4, LPART, MB_SPARSE>
-                          : encode_tma_kernel<PMAX, SM4, LPART, MB>;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem);
-  if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)sms * per_sm;
-  if (grid > nblocks) grid = nblocks;
-  count_launch();
-  kern<<<(unsigned)grid, 128, smem, stream>>>(seqs, nblocks, len, stride, packed, undef);
+struct Enc3Cfg {
+  uint32_t bufb, P;
+  size_t smem;
+};
+
+static Enc3Cfg enc3_cfg(int len, int stride) {
+  Enc3Cfg c;
+  c.bufb = ((uint32_t)(32 * stride + 32) + 127u) & ~127u;
+  uint32_t p = (uint32_t)(5 * len);
+  p = (p + 31u) & ~31u;
+  c.P = p + 16u;  // P = 16 (mod 32): the two planes' transposed writes hit disjoint banks
+  c.smem = (size_t)4 * 2 * c.bufb + (size_t)2 * c.P * 4 + 8 * 8;
+  return c;
 }
 
-template <int PMAX>
-static void dispatch_tma(const uint8_t* seqs, int64_t nblocks, int len, int stride,
-                         uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
-  const bool lpart = (len & 3) != 0;
-  switch (stride & 3) {
-    case 0: lpart ? launch_tma<PMAX, 0, true>(seqs, nblocks, len, stride, packed, undef, stream)
-                  : launch_tma<PMAX, 0, false>(seqs, nblocks, len, stride, packed, undef, stream); break;
-    case 1: lpart ? launch_tma<PMAX, 1, true>(seqs, nblocks, len, stride, packed, undef, stream)
-                  : launch_tma<PMAX, 1, false>(seqs, nblocks, len, stride, packed, undef, stream); break;
-    case 2: lpart ? launch_tma<PMAX, 2, true>(seqs, nblocks, len, stride, packed, undef, stream)
-                  : launch_tma<PMAX, 2, false>(seqs, nblocks, len, stride, packed, undef, stream); break;
-    default: lpart ? launch_tma<PMAX, 3, true>(seqs, nblocks, len, stride, packed, undef, stream)
-                   : launch_tma<PMAX, 3, false>(seqs, nblocks, len, stride, packed, undef, stream); break;
+template <int NCH, bool ALN>
+static void launch_enc3_t(const uint8_t* seqs, int64_t nblocks, int len, int stride,
+                          uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
+  const Enc3Cfg c = enc3_cfg(len, stride);
+  auto kern = encode3_kernel<NCH, ALN, 1>;
+  // launch configuration cached per (device, smem): the attribute and occupancy
+  // queries are host round trips, kept off the per-call path
+  static thread_local int cached_dev = -1, cached_grid = 0;
+  static thread_local size_t cached_smem = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev || c.smem != cached_smem) {
+    if (c.smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, c.smem);
+    cached_grid = sms * (per_sm < 1 ? 1 : per_sm);
+    cached_dev = dev;
+    cached_smem = c.smem;
   }
+  int64_t grid = cached_grid;
+  if (grid > nblocks) grid = nblocks;
+  count_launch();
+  kern<<<(unsigned)grid, 128, c.smem, stream>>>(seqs, nblocks, len, stride, c.bufb, c.P, packed,
+                                                undef);
+}
+
+static void launch_enc3(const uint8_t* seqs, int64_t nblocks, int len, int stride,
+                        uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
+  const int nch = (len + 15) >> 4;
+  const bool aln = (stride & 3) == 0;
+#define GK_ENC3(N)                                                                      \
+  if (nch == N) {                                                                       \
+    if (aln) launch_enc3_t<N, true>(seqs, nblocks, len, stride, packed, undef, stream); \
+    else launch_enc3_t<N, false>(seqs, nblocks, len, stride, packed, undef, stream);    \
+    return;                                                                             \
+  }
+  GK_ENC3(7)   // 97..112 bp (100 bp)
+  GK_ENC3(10)  // 145..160 bp (150 bp)
+  GK_ENC3(16)  // 241..256 bp (250 bp)
+#undef GK_ENC3
+  if (aln) launch_enc3_t<0, true>(seqs, nblocks, len, stride, packed, undef, stream);
+  else launch_enc3_t<0, false>(seqs, nblocks, len, stride, packed, undef, stream);
 }
 
 static void launch_generic(const uint8_t* seqs, int64_t n, int len, int64_t stride,
@@ -229,11 +291,7 @@ int launch_encode(const uint8_t* seqs, int64_t n, int len, int64_t stride, uint3
     // the block holding the last row would read stride-len bytes past the caller's
     // (n-1)*stride+len: that block goes to the generic path, which stops at len
     const int64_t nblocks = stride == len ? n / 128 : (n - 1) / 128;
-    if (nblocks > 0) {
-      if (stride <= 128) dispatch_tma<128>(seqs, nblocks, len, (int)stride, packed, undef, stream);
-      else if (stride <= 256) dispatch_tma<256>(seqs, nblocks, len, (int)stride, packed, undef, stream);
-      else dispatch_tma<512>(seqs, nblocks, len, (int)stride, packed, undef, stream);
-    }
+    if (nblocks > 0) launch_enc3(seqs, nblocks, len, (int)stride, packed, undef, stream);
     first_generic = nblocks * 4;
   }
   launch_generic(seqs, n, len, stride, packed, undef, first_generic, stream);

@@ -1,0 +1,127 @@
+// gk_encode3.cuh -- a1 (ASCII -> bit-sliced 2-bit planes) at a few instructions per
+// byte: the group's 32 rows are staged in shared memory (one TMA bulk copy);
+// every lane extracts the code bits of 4 rows x 4 bytes per 16-position chunk
+// into one 32-bit word and a 3-stage shuffle transpose turns the 32 lanes' words
+// into 32 "position x plane" words of the packed layout (bit j = row j).
+//
+// Per 4 bytes w of a row (SWAR, branch-free):
+//  * code planes (A=00 C=01 G=10 T=11): for A C G T a c g t the
+//    ASCII bit 2 is the high code bit and bit 1 ^ bit 2 the low one; bit 3 is 0,
+//    so x = (w ^ (w >> 1)) & 0x06 per byte holds low at bit 1, high at bit 2.
+//  * validity (reading R8): a byte is one of the 8 letters iff
+//      bits 7,6,3 = 0,1,0        -> (w ^ 0x40) & 0xC8 == 0
+//      b4 == b2 & ~b1, b0 != b4  -> bit 4 of  (w ^ (w<<2 & ~(w<<3))) | ~(w ^ w<<4)  == 0
+//    (the 8 solutions are exactly 0x41 43 47 54 61 63 67 74).  Both tests are
+//    ORed into per-row accumulators unmasked (OR commutes with the final mask).
+//  The shifts left are IMADs (FMA pipe), the rest one LOP3 each (ALU pipe).
+//
+// Lane layout.  Lane l = cw + 4*rh (cw = 0..3: the lane's 4-byte column of the
+// 16-byte chunk; rh = 0..7) holds rows r_i = rh0 + 2i + 8 rh1 + 16 rh2 (i = 0..3):
+// rows spaced by 2, so that the transpose ends with bit r = row r (below).  The
+// lane's merged word has bit t = b' + 2i + 8k for byte k (position 4cw+k) of row
+// i, plane b' (0: low, 1: high).  A 32x32 transpose would take 5 shuffle stages;
+// the load pattern already performed two of them (lane bits 0-1 = the column
+// block), and 3 stages swap lane bits 2,3,4 with bit-index bits 0,3,4:
+// afterwards lane l = cw + 4b' + 8k holds one position x plane word whose bit
+// t = rh0 + 2i + 8rh1 + 16rh2 = r is row r.  Each stage is SHFL + SHF (rotate)
+// + LOP3 (select).
+#pragma once
+#include "gk_common.cuh"
+#include "gk_tma.cuh"
+
+namespace gk {
+namespace enc3 {
+
+// FMA-pipe shifts (ptxas keeps mul.lo by a register as IMAD)
+__device__ __forceinline__ uint32_t imul(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t imadhi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t lop3_or(uint32_t a, uint32_t b, uint32_t c) {
+  return a | b | c;
+}
+
+// Per-lane constants.
+struct Lane {
+  uint32_t m2, m4, m8, m16, m32, mh;  // multipliers in registers (keep them IMADs)
+  uint32_t keep[3];                   // select masks of the 3 transpose stages
+  uint32_t rot[3];                    // rotate amounts
+  int rows[4];                        // r_i
+  int cw;
+  __device__ __forceinline__ void init(int lane) {
+    m2 = 2u; m4 = 4u; m8 = 8u; m16 = 16u; m32 = 32u; mh = 0x80000000u;
+    cw = lane & 3;
+    const int rh0 = (lane >> 2) & 1, rh1 = (lane >> 3) & 1, rh2 = (lane >> 4) & 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rows[i] = rh0 + 2 * i + 8 * rh1 + 16 * rh2;
+    // stage s swaps lane bit LB[s] with bit-index bit TB[s]
+    const int LB[3] = {2, 3, 4}, TB[3] = {0, 3, 4};
+    const uint32_t Z[3] = {0x55555555u, 0x00FF00FFu, 0x0000FFFFu};  // bit-index bit TB = 0
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const bool up = (lane >> LB[s]) & 1;
+      keep[s] = up ? ~Z[s] : Z[s];
+      rot[s] = up ? 32u - (1u << TB[s]) : (1u << TB[s]);
+    }
+  }
+};
+
+// 32x32 transpose tail: 3 stages (lane bits 2,3,4 <-> bit-index bits 0,3,4).
+__device__ __forceinline__ uint32_t transpose3(uint32_t m, const Lane& ln) {
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, m, 4 << s);
+    const uint32_t r = __funnelshift_l(y, y, ln.rot[s]);
+    m = (m & ln.keep[s]) | (r & ~ln.keep[s]);
+  }
+  return m;
+}
+
+// One row's 4 bytes: validity accumulators and the plane bits (low at bit 1,
+// high at bit 2 of every byte).
+__device__ __forceinline__ uint32_t row_word(uint32_t w, const Lane& ln, uint32_t& acc_g,
+                                             uint32_t& acc_y) {
+  const uint32_t s2 = imul(w, ln.m4), s3 = imul(w, ln.m8), s4 = imul(w, ln.m16);
+  const uint32_t h = w ^ (s2 & ~s3);
+  const uint32_t g = h | ~(w ^ s4);
+  acc_g |= g;
+  acc_y |= w ^ 0x40404040u;
+  const uint32_t sh = imadhi(w, ln.mh, 0u);  // w >> 1 on the FMA pipe
+  return (w ^ sh) & 0x06060606u;
+}
+
+// Merge the 4 rows' plane bits: bit t = b' + 2i + 8k.
+__device__ __forceinline__ uint32_t merge4(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3,
+                                           const Lane& ln) {
+  uint32_t m = imadhi(x0, ln.mh, 0u);  // >> 1
+  m = imad(x1, ln.m2, m);              // << 1
+  m = imad(x2, ln.m8, m);              // << 3
+  m = imad(x3, ln.m32, m);             // << 5
+  return m;
+}
+
+// Row flags of the lane -> the group's undefined word (bit r = row r).
+__device__ __forceinline__ uint32_t group_undef(const uint32_t (&ag)[4], const uint32_t (&ay)[4],
+                                                const Lane& ln) {
+  uint32_t u = 0u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool bad = ((ag[i] & 0x10101010u) | (ay[i] & 0xC8C8C8C8u)) != 0u;
+    u |= bad ? (1u << ln.rows[i]) : 0u;
+  }
+  return __reduce_or_sync(0xFFFFFFFFu, u);
+}
+
+}  // namespace enc3
+}  // namespace gk

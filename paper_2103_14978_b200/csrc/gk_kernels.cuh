@@ -28,7 +28,9 @@ int launch_filter_ascii(const uint8_t* reads, const uint8_t* refs, int64_t strid
                         int len, int e, uint32_t* accept, uint8_t* errc, cudaStream_t stream);
 
 size_t compact_workspace_bytes(int64_t n, int rows = 1);
+// ibase is added to every written index (chunked host pipelines: absolute indices)
 int launch_compact(const uint32_t* bits, int64_t n, uint32_t* idx, uint64_t* n_acc, void* ws,
-                   cudaStream_t stream, int rows = 1, int64_t bstride = 0, int64_t istride = 0);
+                   cudaStream_t stream, int rows = 1, int64_t bstride = 0, int64_t istride = 0,
+                   uint32_t ibase = 0);
 
 }  // namespace gk

@@ -47,7 +47,7 @@ def test_size_queries(lib):
     assert lib.gk_result_words(33) == 2
     assert lib.gk_result_words(0) == 0
     assert lib.gk_compact_workspace_bytes(1) >= 4
-    assert lib.gk_host_workspace_bytes(1024, 100) > 2 * 1024 * 100
+    assert lib.gk_host_workspace_bytes(1024, 100, 100) > 2 * 1024 * 100
 
 
 def test_status_strings(lib):
@@ -103,17 +103,28 @@ def test_argument_validation_before_any_launch(lib):
     assert lib.gk_gather_windows(P + 8, 1000, P, 10, 100, P, P, None) == -4  # planes
     assert lib.gk_gather_windows(P, 1000, None, 10, 100, P, P, None) == -1
     assert lib.gk_host_index_workspace_bytes(1024, 100, 10) > 2 * 1024 * 16
-    assert lib.gk_filter_host_index(P, 10, P, 10, P, P, 10, 100, 100, P, None, P, 1 << 30, 1024) == -3
-    assert lib.gk_filter_host_index(P, 10, P, 10, P, P, 10, 100, 5, P, None, P, 1 << 30, 1000) == -1
-    assert lib.gk_filter_host_index(P, 10, P, 10, P, P, 10, 100, 5, P, None, P, 10, 1024) == -5
-    assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 1 << 30, 1000) == -1  # chunk
-    assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, 10, 1024) == -5
+    assert lib.gk_filter_host_index(P, 10, P, 10, P, P, 10, 100, 100, P, None, P, 1 << 30, 1024,
+                                    None) == -3
+    assert lib.gk_filter_host_index(P, 10, P, 10, P, P, 10, 100, 5, P, None, P, 1 << 30, 1000,
+                                    None) == -1
+    assert lib.gk_filter_host_index(P, 10, P, 10, P, P, 10, 100, 5, P, None, P, 10, 1024,
+                                    None) == -5
+    assert lib.gk_host_workspace_bytes(1024, 100, 100) > 2 * 1024 * 100
+    assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, None, None, P, 1 << 30, 1000,
+                              None) == -1  # chunk
+    assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, None, None, P, 10, 1024, None) == -5
+    # indices need a count; neither accept bits nor indices is an error
+    assert lib.gk_filter_host(P, P, 100, 10, 100, 2, P, None, P, None, P, 1 << 30, 1024,
+                              None) == -1
+    assert lib.gk_filter_host(P, P, 100, 10, 100, 2, None, None, None, None, P, 1 << 30, 1024,
+                              None) == -1
     import ctypes as C
     es = (C.c_int32 * 2)(1, 100)
-    assert lib.gk_filter_host_sweep(P, P, 100, 10, 100, es, 2, P, None, P, 1 << 30, 1024) == -3
+    assert lib.gk_filter_host_sweep(P, P, 100, 10, 100, es, 2, P, None, P, 1 << 30, 1024,
+                                    None) == -3
     es = (C.c_int32 * 2)(1, 5)
-    assert lib.gk_filter_host_sweep(P, P, 100, 10, 100, es, 2, P, None, P, 10, 1024) == -5
-    assert lib.gk_filter_host_sweep(P, P, 100, 10, 100, es, 0, P, None, P, 10, 1024) == -1
+    assert lib.gk_filter_host_sweep(P, P, 100, 10, 100, es, 2, P, None, P, 10, 1024, None) == -5
+    assert lib.gk_filter_host_sweep(P, P, 100, 10, 100, es, 0, P, None, P, 10, 1024, None) == -1
 
 
 def test_product_package_does_not_import_the_oracle():

@@ -496,10 +496,50 @@ def test_filter_host_end_to_end(gk):
     hr = torch.from_numpy(reads).pin_memory()
     hf = torch.from_numpy(refs).pin_memory()
     err = torch.empty(n, dtype=torch.uint8).pin_memory()
-    acc, _ = gk.filter_host(hr, hf, 5, errcount=err, chunk_pairs=8192)
+    acc, _, _ = gk.filter_host(hr, hf, 5, errcount=err, chunk_pairs=8192)
     oa, oc = oracle.filter(reads, refs, 5)
     assert (unpack_accept(acc, n) == oa).all()
     assert (err.numpy() == oc).all()
+
+
+@pytest.mark.parametrize("n,chunk", [(50_000, 8192), (4097, 1024), (1024, 2048), (70_001, 16384)])
+def test_filter_host_indices(gk, n, chunk):
+    """The host pipeline's compaction stage (NEXT-2): per chunk gk_compact with an index
+    base, counts drained while the next chunk runs -> one ascending list of accepted
+    pairs, equal to the oracle's; accept bits of the same call agree too."""
+    L, e = 100, 5
+    reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, emax=e)
+    hr = torch.from_numpy(reads).pin_memory()
+    hf = torch.from_numpy(refs).pin_memory()
+    acc, _, idx = gk.filter_host(hr, hf, e, indices=True, chunk_pairs=chunk)
+    oa, _ = oracle.filter(reads, refs, e)
+    expect = np.nonzero(oa)[0]
+    assert idx.numel() == expect.size
+    assert (idx.to(torch.int64).numpy() == expect).all()
+    assert (unpack_accept(acc, n) == oa).all()
+    # indices only (no accept bits)
+    _, _, idx2 = gk.filter_host(hr, hf, e, indices=True, want_accept=False, chunk_pairs=chunk)
+    assert (idx2.to(torch.int64).numpy() == expect).all()
+
+
+def test_filter_host_waits_for_the_callers_stream(gk):
+    """the pipeline must not race work still queued on the caller's stream.
+    The host inputs are fine, so race the device workspace: a kernel on the current
+    stream fills it with junk right before the call; the call must order itself after
+    it (an event recorded on the stream) -- results stay exact."""
+    n, L, e = 20_000, 100, 4
+    reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, emax=e)
+    hr = torch.from_numpy(reads).pin_memory()
+    hf = torch.from_numpy(refs).pin_memory()
+    ws = torch.empty(gk.host_workspace_bytes(4096, L, L), dtype=torch.uint8, device="cuda")
+    oa, _ = oracle.filter(reads, refs, e)
+    for _ in range(3):
+        big = torch.empty(1 << 26, dtype=torch.float32, device="cuda")
+        for _ in range(20):
+            big.mul_(1.0001)  # keep the current stream busy
+        ws.fill_(0xAB)        # queued behind the busy work, then the call reuses ws
+        acc, _, _ = gk.filter_host(hr, hf, e, workspace=ws, chunk_pairs=4096)
+        assert (unpack_accept(acc, n) == oa).all()
 
 
 def test_filter_host_sweep(gk):

@@ -34,8 +34,9 @@ for L, n in [(100, 3000), (150, 2200), (37, 1500)]:
     gk.accuracy(a2, e2, d, n, range(5))
     gk.compact_rows(a2, n)
     torch.cuda.synchronize()
-    acc, _ = gk.filter_host(torch.from_numpy(hr).pin_memory(), torch.from_numpy(hf).pin_memory(),
-                            4, chunk_pairs=1024)
+    acc, _, _ = gk.filter_host(torch.from_numpy(hr).pin_memory(),
+                               torch.from_numpy(hf).pin_memory(), 4, indices=True,
+                               chunk_pairs=1024)
     gk.filter_host_sweep(torch.from_numpy(hr), torch.from_numpy(hf), [0, 5], chunk_pairs=1024)
 torch.cuda.synchronize()
 print("sanitize_run ok")
