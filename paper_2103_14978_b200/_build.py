@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libgk.so")
 SOURCES = ["gk_api.cu", "gk_encode.cu", "gk_filter.cu", "gk_filter_ascii.cu", "gk_compact.cu",
            "gk_filter_ascii_p0.cu", "gk_filter_ascii_p1.cu", "gk_filter_ascii_p2.cu",
-           "gk_filter_ascii_p3.cu", "gk_filter_bt.cu", "gk_verify.cu", "gk_index.cu"]
+           "gk_filter_ascii_p3.cu", "gk_filter_bt.cu", "gk_filter_bt2.cu", "gk_verify.cu", "gk_index.cu"]
 HEADERS = ["gk_common.cuh", "gk_kernels.cuh", "gk_encode_core.cuh", "gk_filter_core.cuh",
            "gk_tma.cuh", "gk_filter_ascii_impl.cuh", "gk_encode3.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -31,13 +31,22 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in _inputs())
 
 
-def build(verbose: bool = False, force: bool = False, jobs: int | None = None) -> str:
-    if not force and not stale():
+def build(verbose: bool = False, force: bool = False, jobs: int | None = None,
+          defines=(), out: str | None = None) -> str:
+    """Build libgk.so (or, with `defines` such as ["GK_BT2=0"], an A/B variant at `out`)."""
+    so = out or SO
+    if not force and not defines and not stale():
         return SO
-    objdir = os.path.join(HERE, "build")
+    if defines and os.path.exists(so) and not force:
+        t = os.path.getmtime(so)
+        if all(os.path.getmtime(f) <= t for f in _inputs()):
+            return so
+    objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(
+        d.replace("=", "") for d in defines))
     os.makedirs(objdir, exist_ok=True)
     common = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+    common += [f"-D{d}" for d in defines]
     if verbose:
         common += ["-Xptxas", "-v"]
     procs, objs = [], []
@@ -58,9 +67,9 @@ def build(verbose: bool = False, force: bool = False, jobs: int | None = None) -
     if failed:
         raise RuntimeError("libgk.so build failed")
     link = ["nvcc", *ARCH, "-shared", "-cudart", "shared", "-Xlinker",
-            "-rpath,/usr/local/cuda/lib64", "-o", SO, *objs]
+            "-rpath,/usr/local/cuda/lib64", "-o", so, *objs]
     subprocess.check_call(link)
-    return SO
+    return so
 
 
 if __name__ == "__main__":
