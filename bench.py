@@ -76,8 +76,10 @@ def parse(argv=None):
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c5", choices=["c2", "c3", "c4", "c5"])
-    p.add_argument("--path", default=None,
-                   help="c5: packed (default) | fused;  c2-c4: sweep (default) | packed | fused")
+    p.add_argument("--path", default="auto", choices=["auto", "fused", "packed", "per-e"],
+                   help="auto (default): fused kernels for reads <= 192 bp, encode + filter "
+                        "kernels above; fused | packed: force one; per-e (c2-c4): one "
+                        "gk_filter launch per threshold instead of the one-pass sweep")
     p.add_argument("--total", type=int, default=None, help="c5: total pairs (default 1B)")
     p.add_argument("--n", type=int, default=None, help="c2-c4: pairs per GPU (default 30M)")
     p.add_argument("--mem-gb", type=float, default=110.0,
@@ -89,10 +91,17 @@ def parse(argv=None):
     p.add_argument("--no-alt", action="store_true", help="c2-c4: skip the per-e comparison path")
     p.add_argument("--cpu-budget", type=float, default=20.0,
                    help="seconds of host work for the oracle baseline")
-    a = p.parse_args(argv)
-    if a.path is None:
-        a.path = "packed" if a.config == "c5" else "sweep"
-    return a
+    return p.parse_args(argv)
+
+
+def path_of(args, L):
+    from paper_2103_14978_b200.pipeline import auto_path
+    if args.path == "auto":
+        return auto_path(L)
+    return "packed" if args.path == "per-e" else args.path
+
+
+PATH_DESC = {"fused": "fused ASCII kernel", "packed": "gk_encode x2 + filter kernel"}
 
 
 # ---------------------------------------------------------------------------
@@ -121,9 +130,10 @@ def config_of(args, world):
         return {"workload": f"c5: {total} pairs, 100/150/250 bp thirds, e = 5/7/12 "
                             f"(BASELINE configs[{wl.config_index}]), split evenly over the ranks",
                 "total_pairs": total,
-                "buckets": [{"read_len": L, "e": es[0], "pairs": n} for L, es, _, n in bk],
-                "path": {"fused": "gk_filter_ascii + gk_compact per bucket",
-                         "packed": "gk_encode x2 + gk_filter + gk_compact per bucket"}[args.path],
+                "buckets": [{"read_len": L, "e": es[0], "pairs": n,
+                             "path": {"fused": "gk_filter_ascii + gk_compact",
+                                      "packed": "gk_encode x2 + gk_filter + gk_compact"}[
+                                 path_of(args, L)]} for L, es, _, n in bk],
                 "profile": "paper", "seed": SEED,
                 "l2": "inputs >= 6.6 GB per resident chunk > 126 MB L2 (no flush needed)",
                 "parallelism": f"dp{world} (pairs sharded, no data-path collective)"}
@@ -131,9 +141,11 @@ def config_of(args, world):
     return {"workload": f"{args.config}: {n} pairs x {L} bp per GPU, e swept {es[0]}..{es[-1]} "
                         f"(BASELINE configs[{wl.config_index}])",
             "n_pairs_per_gpu": n, "read_len": L, "e": f"{es[0]}-{es[-1]}",
-            "path": {"fused": "gk_filter_ascii + gk_compact per e",
-                     "packed": "gk_encode x2 + (gk_filter + gk_compact) per e",
-                     "sweep": "gk_encode x2 + gk_filter_sweep + gk_compact_rows (all e)"}[args.path],
+            "path": ("gk_encode x2 + (gk_filter + gk_compact) per e" if args.path == "per-e" else
+                     {"fused": "gk_filter_ascii_sweep (encode + all e in one kernel) + "
+                               "gk_compact_rows",
+                      "packed": "gk_encode x2 + gk_filter_sweep (all e in one pass) + "
+                                "gk_compact_rows"}[path_of(args, L)]),
             "profile": "paper", "seed": SEED,
             "l2": f"inputs {2 * n * L / 1e9:.1f} GB per GPU > 126 MB L2 (no flush needed)",
             "parallelism": f"dp{world} (pairs sharded, no data-path collective)"}
@@ -383,6 +395,7 @@ def run_dry(args):
 def alg_bytes(kernel, L, es):
     rows = len(es)
     return {"filter_ascii": 2 * L + 1 / 8 + 1,
+            "filter_ascii_sweep": 2 * L + rows * (1 / 8 + 1),
             "encode": 2 * (L + L / 4) + 2 / 8,
             "filter": L / 2 + 2 / 8 + 1 / 8 + 1,
             "filter_sweep": L / 2 + 2 / 8 + rows * (1 / 8 + 1),
@@ -398,7 +411,7 @@ def alg_ops(kernel, L, es):
     cells = L * (2 * e + 1) - e * (e + 1)
     if kernel in ("filter", "filter_ascii"):
         return (5 * cells + 8 * L) / 32.0
-    if kernel == "filter_sweep":
+    if kernel in ("filter_sweep", "filter_ascii_sweep"):
         return (5 * cells + 4 * L * (e + 2)) / 32.0
     return 0.0
 
@@ -454,7 +467,7 @@ def run_buckets(args, ctx):
     plan = []
     for L, es, idx0, n in bk:
         lo, cnt = sharding.even_shard(n, rank, world) if c5 else sharding.weak_shard(n, rank)
-        per_pair = 2 * L + 8 + len(es) * 6 + (L // 2 if args.path != "fused" else 0)
+        per_pair = 2 * L + 8 + len(es) * 6 + (L // 2 if path_of(args, L) == "packed" else 0)
         cap = max(1024, int(args.mem_gb * 1e9 / per_pair) // 1024 * 1024)
         nch = (cnt + cap - 1) // cap
         size = (cnt + nch - 1) // nch
@@ -483,11 +496,10 @@ def run_buckets(args, ctx):
     sampler_started = False
     for ci, (L, es, p0, m) in enumerate(plan):
         reads, refs = pairgen.gen_pairs_cuda(m, L, idx0=p0, device=dev)
-        if c5 or args.path != "sweep":
-            steps_obj = [BucketStep(torch, m, L, e, dev, path="fused" if args.path == "fused"
-                                    else "packed") for e in es]
+        if c5 or args.path == "per-e":
+            steps_obj = [BucketStep(torch, m, L, e, dev, path=path_of(args, L)) for e in es]
         else:
-            steps_obj = [SweepStep(torch, m, L, es[-1], dev)]
+            steps_obj = [SweepStep(torch, m, L, es[-1], dev, path=path_of(args, L))]
         torch.cuda.synchronize(dev)
 
         def one(record=False):
@@ -537,7 +549,7 @@ def run_buckets(args, ctx):
             acc_rows = s.n_acc.tolist()
             for j, e in enumerate(s.es if hasattr(s, "es") else es):
                 accepted[f"{key}:{e}"] = accepted.get(f"{key}:{e}", 0) + int(acc_rows[j])
-        if not c5 and args.path == "sweep" and ci == len(plan) - 1:
+        if not c5 and args.path != "per-e" and ci == len(plan) - 1:
             # the paper's accuracy study (Tables S.2-S.6) on the whole batch, after the timed
             # region: exact edit distance on the device vs the sweep's decisions
             st = steps_obj[0]
@@ -563,7 +575,7 @@ def run_buckets(args, ctx):
     value = work / (ms_all / 1e3) / 1e9
 
     # roofline of every kernel family; the dominant one is the largest share of the step
-    ncu = load_ncu(f"{args.config}:{args.path}")
+    ncu = load_ncu(f"{args.config}:{args.path}")  # profiles/r*_traffic.json of this workload
     kernels = []
     for kname, kms in kern_ms.items():
         b, o, parts = kern_work[kname]

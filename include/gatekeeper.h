@@ -158,6 +158,19 @@ int gk_filter_ascii(const uint8_t* d_reads, const uint8_t* d_refs, int64_t strid
                     int64_t n_pairs, int32_t len, int32_t e,
                     uint32_t* d_accept_bits, uint8_t* d_errcount, void* stream);
 
+/* a1-a6 for EVERY threshold e = 0..e_max in one launch from ASCII: the encode of
+ * gk_filter_ascii and the one-pass sweep of gk_filter_sweep fused (one CTA per
+ * tile of 1024 pairs; the 2-bit planes stay in shared memory).  Outputs as
+ * gk_filter_sweep (row e = threshold e; row stride gk_result_words(n_pairs)
+ * words / n_pairs bytes).
+ *  d_reads, d_refs : 16-byte aligned (else GK_ERR_ALIGN).
+ * Errors: as gk_filter_ascii; GK_ERR_LEN also when the tile and the per-e
+ * counters do not fit in shared memory (about len * 512 + e_max * 3.5 KB bytes
+ * > 227 KB, e.g. 250 bp with e_max = 25): use gk_encode + gk_filter_sweep. */
+int gk_filter_ascii_sweep(const uint8_t* d_reads, const uint8_t* d_refs, int64_t stride,
+                          int64_t n_pairs, int32_t len, int32_t e_max,
+                          uint32_t* d_accept_bits, uint8_t* d_errcount, void* stream);
+
 /* a7: ordered indices of the accepted pairs (the accepted
  * pairs go on to verification).
  *  d_accept_bits : as written by gk_filter for n_pairs (n_pairs < 2^32).

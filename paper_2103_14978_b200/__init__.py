@@ -56,6 +56,7 @@ def load_library(path: str = LIB_PATH):
         "gk_filter_ex": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, I32, P]),
         "gk_filter_sweep": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, I32, P]),
         "gk_filter_ascii": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P]),
+        "gk_filter_ascii_sweep": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P]),
         "gk_compact_workspace_bytes": (SZ, [I64]),
         "gk_compact": (ctypes.c_int, [P, I64, P, P, P, SZ, P]),
         "gk_compact_rows_workspace_bytes": (SZ, [I64, I32]),
@@ -183,6 +184,25 @@ def filter_ascii(reads, refs, e: int, length: int | None = None, accept=None, er
     _check(load_library().gk_filter_ascii(reads.data_ptr(), refs.data_ptr(), stride, n, length,
                                           e, _ptr(accept), _ptr(errcount), _stream(stream)),
            "gk_filter_ascii")
+    return accept, errcount
+
+
+def filter_ascii_sweep(reads, refs, e_max: int, length: int | None = None, accept=None,
+                       errcount=None, want_errcount: bool = True, stream=None):
+    """Fused a1..a6 for every e = 0..e_max from ASCII rows -> (accept bits [e_max+1, words],
+    errcount [e_max+1, n] or None); row e equals filter_ascii(..., e)."""
+    import torch
+    n, stride = reads.shape
+    length = stride if length is None else length
+    rows = e_max + 1
+    if accept is None:
+        accept = torch.empty((rows, max(1, result_words(n))), dtype=torch.int32,
+                             device=reads.device)
+    if errcount is None and want_errcount:
+        errcount = torch.empty((rows, max(1, n)), dtype=torch.uint8, device=reads.device)
+    _check(load_library().gk_filter_ascii_sweep(reads.data_ptr(), refs.data_ptr(), stride, n,
+                                                length, e_max, _ptr(accept), _ptr(errcount),
+                                                _stream(stream)), "gk_filter_ascii_sweep")
     return accept, errcount
 
 

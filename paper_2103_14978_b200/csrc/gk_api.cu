@@ -155,6 +155,23 @@ int gk_filter_ascii(const uint8_t* d_reads, const uint8_t* d_refs, int64_t strid
   return after_launch();
 }
 
+int gk_filter_ascii_sweep(const uint8_t* d_reads, const uint8_t* d_refs, int64_t stride,
+                          int64_t n_pairs, int32_t len, int32_t e_max, uint32_t* d_accept_bits,
+                          uint8_t* d_errcount, void* stream) {
+  int rc = check_ascii(d_reads, n_pairs, len, stride);
+  if (rc) return rc;
+  if (n_pairs > 0 && d_refs == nullptr) return GK_ERR_ARG;
+  if (e_max < 0 || e_max >= len) return GK_ERR_E;
+  if (n_pairs == 0) return GK_OK;
+  if (!d_accept_bits) return GK_ERR_ARG;
+  if (!aligned(d_accept_bits, 4)) return GK_ERR_ALIGN;
+  if (!aligned(d_reads, 16) || !aligned(d_refs, 16)) return GK_ERR_ALIGN;
+  if (!gk::launch_fused(d_reads, d_refs, stride, n_pairs, len, e_max, true, d_accept_bits,
+                        d_errcount, (cudaStream_t)stream))
+    return GK_ERR_LEN;  // the tile does not fit in shared memory: gk_encode + gk_filter_sweep
+  return after_launch();
+}
+
 size_t gk_compact_workspace_bytes(int64_t n_pairs) {
   return gk::compact_workspace_bytes(n_pairs < 0 ? 0 : n_pairs);
 }

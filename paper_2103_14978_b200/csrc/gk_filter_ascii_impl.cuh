@@ -1,4 +1,6 @@
-// gk_filter_ascii_impl.cuh -- a1..a6 fused: ASCII pairs -> accept bits / error counts.
+// gk_filter_ascii_impl.cuh -- a1..a6 fused, generic fallback: the kernel behind
+// gk_filter_ascii when the tile-per-CTA kernels of gk_fused.cu do not fit in
+// shared memory (long reads) or the inputs are not 16-byte aligned.
 //
 // The paper's "device-encoded" kernel encodes each pair inside the filtering
 // thread.  Here one CTA (4 warps) owns G groups (G*32 pairs, a
@@ -159,176 +161,6 @@ __global__ void __launch_bounds__(128) filter_ascii_kernel(
   }
 }
 
-// ---------------------------------------------------------------------------
-// TMA version: CTA = 4 warps, G = 32 groups (one tile of 1024 pairs).  Phase 1:
-// warp w encodes groups w, w+4, ...; the 32 read rows and the 32 reference rows
-// of a group are each one contiguous span brought in by cp.async.bulk, two
-// buffers per warp alternating between the read span and the reference span so
-// that the next span lands while the current one is encoded.  The encoder is
-// the one of gk_encode (encode_group_v2), emitting into the shared packed tile.
-// Phase 2 as in the generic kernel.
-template <int SM4, bool LPART, int NIT, uint32_t BUFB>
-__device__ __forceinline__ void ascii_phase1(const uint8_t* __restrict__ reads,
-                                             const uint8_t* __restrict__ refs, int stride,
-                                             int len, int64_t gbase, uint2* pq, uint2* pr,
-                                             uint32_t* und, uint8_t* stg, uint32_t buf_bytes,
-                                             uint64_t* bars, int P) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t span = 32u * (uint32_t)stride;
-  RowAddr<SM4> ra;
-  ra.init(smem_u32(stg), (uint32_t)stride, lane);
-  // span sequence: (g0 reads -> buf0), (g0 refs -> buf1), (g1 reads -> buf0), ...
-  auto issue = [&](int k) {  // k-th span of this warp
-    const int gl = warp + 4 * (k >> 1);
-    const uint8_t* src = ((k & 1) ? refs : reads) + (gbase + gl) * (int64_t)span;
-    uint64_t* bar = &bars[k & 1];
-    fence_proxy_async();
-    mbar_arrive_expect_tx(bar, span);
-    tma_load_1d(stg + (k & 1) * buf_bytes, src, span, bar);
-  };
-  constexpr int NSPAN = 2 * 8;  // 8 groups per warp (G = 32), 2 spans each
-  if (lane == 0) {
-    issue(0);
-    issue(1);
-  }
-  uint32_t u = 0u;
-#pragma unroll 1
-  for (int k = 0; k < NSPAN; ++k) {
-    const int b = k & 1;
-    mbar_wait(&bars[b], (uint32_t)(k >> 1) & 1u);
-    const int gl = warp + 4 * (k >> 1);
-    uint2* dst = (b ? pr : pq) + gl;
-    auto emit = [&](int q, int m, uint32_t hi, uint32_t lo) { dst[(4 * q + m) * P] = make_uint2(hi, lo); };
-    const uint32_t uu = b == 0 ? encode_group_v2<SM4, LPART, NIT, 0u>(ra, len, emit)
-                               : encode_group_v2<SM4, LPART, NIT, BUFB>(ra, len, emit);
-    u |= uu;
-    if (b) {
-      if (lane == 0) und[gl] = u;
-      u = 0u;
-    }
-    __syncwarp();
-    if (lane == 0 && k + 2 < NSPAN) issue(k + 2);
-  }
-}
-
-template <int E, int PMAX>
-__global__ void __launch_bounds__(128) filter_ascii_tma_kernel(
-    const uint8_t* __restrict__ reads, const uint8_t* __restrict__ refs, int stride,
-    int64_t ntiles_full, int64_t n, int len, int e, uint32_t* __restrict__ accept,
-    uint8_t* __restrict__ errc) {
-  constexpr int G = 32, P = G + 1;
-  constexpr uint32_t BUF = 32u * PMAX;
-  constexpr int NIT = PMAX / 128;
-  extern __shared__ __align__(128) uint8_t sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* stg = sm;                                              // [4 warps][2][BUF]
-  uint2* pq = reinterpret_cast<uint2*>(sm + 4 * 2 * BUF);        // [len][P]
-  uint2* pr = pq + (size_t)len * P;
-  uint32_t* und = reinterpret_cast<uint32_t*>(pr + (size_t)len * P);  // [32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(und + 32) + 2 * warp;
-  if (lane == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  const int64_t tile = blockIdx.x;
-  if (tile >= ntiles_full) return;
-  const int64_t gbase = tile * G;
-  uint8_t* mystg = stg + (size_t)warp * 2 * BUF;
-  const bool lpart = (len & 3) != 0;
-  switch ((stride & 3) * 2 + (lpart ? 1 : 0)) {
-    case 0: ascii_phase1<0, false, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 1: ascii_phase1<0, true, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 2: ascii_phase1<1, false, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 3: ascii_phase1<1, true, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 4: ascii_phase1<2, false, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 5: ascii_phase1<2, true, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    case 6: ascii_phase1<3, false, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-    default: ascii_phase1<3, true, NIT, BUF>(reads, refs, stride, len, gbase, pq, pr, und, mystg, BUF, bars, P); break;
-  }
-  __syncthreads();
-
-  const int64_t g = gbase + lane;
-  SmemGroupSrc src;
-  src.q = pq + lane;
-  src.r = pr + lane;
-  src.len = len;
-  src.pstride = P;
-  if constexpr (E >= 0) {
-    int chunk = (len + 3) / 4;
-    chunk = (chunk + 3) & ~3;
-    const int lo = warp * chunk;
-    int hi = lo + chunk;
-    if (hi > len) hi = len;
-    uint32_t cA[8], cF[8];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) cA[b] = cF[b] = 0u;
-    if (lo < hi) {
-      SinglePass<E> sp;
-      run_range<E>(sp, src, len, lo, hi);
-      sp.cA.planes(cA);
-      sp.cF.planes(cF);
-    }
-    uint32_t* xch = reinterpret_cast<uint32_t*>(stg);  // staging is free now
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      xch[(warp * 16 + b) * 32 + lane] = cA[b];
-      xch[(warp * 16 + 8 + b) * 32 + lane] = cF[b];
-    }
-    __syncthreads();
-    if (warp == 0) {
-      for (int w = 1; w < 4; ++w) {
-        add_planes(cA, xch + (w * 16) * 32 + lane, 32);
-        add_planes(cF, xch + (w * 16 + 8) * 32 + lane, 32);
-      }
-      finish_group(cA, cF, e, und[lane], g, n, accept, errc);
-    }
-  } else {
-    if (warp == 0) {
-      uint32_t cA[8], cF[8];
-      uint32_t* Fsm = reinterpret_cast<uint32_t*>(stg);  // [len][32] fits in the staging area
-      generic_group(src, len, e, und[lane], Fsm + lane, 32, cA, cF);
-      finish_group(cA, cF, e, und[lane], g, n, accept, errc);
-    }
-  }
-}
-
-template <int E, int PMAX>
-static void launch_ascii_tma(const uint8_t* reads, const uint8_t* refs, int stride,
-                             int64_t ntiles, int64_t n, int len, int e, uint32_t* accept,
-                             uint8_t* errc, cudaStream_t stream) {
-  const size_t smem = (size_t)4 * 2 * 32 * PMAX + 2 * (size_t)len * 33 * 8 + 32 * 4 + 4 * 2 * 8 + 16;
-  auto kern = filter_ascii_tma_kernel<E, PMAX>;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  count_launch();
-  kern<<<(unsigned)ntiles, 128, smem, stream>>>(reads, refs, stride, ntiles, n, len, e, accept,
-                                                errc);
-}
-
-// returns the number of tiles handled by the TMA kernel
-template <int E>
-static int64_t try_ascii_tma(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n,
-                             int len, int e, uint32_t* accept, uint8_t* errc,
-                             cudaStream_t stream) {
-  if (!GK_ASCII_TMA) return 0;
-  if (((reinterpret_cast<uintptr_t>(reads) | reinterpret_cast<uintptr_t>(refs)) & 15u) != 0)
-    return 0;
-  // a tile copies 1024*stride bytes per set: with stride > len the tile holding the
-  // last row would over-read the caller's (n-1)*stride+len bytes -> generic path
-  const int64_t ntiles = stride == len ? n / 1024 : (n - 1) / 1024;
-  if (ntiles == 0) return 0;
-  // the generic fallback (E < 0) keeps F[len][32] in the staging area
-  if (E < 0 && (size_t)len * 32 * 4 > (size_t)4 * 2 * 32 * (stride <= 128 ? 128 : stride <= 256 ? 256 : 512))
-    return 0;
-  if (stride <= 128) launch_ascii_tma<E, 128>(reads, refs, (int)stride, ntiles, n, len, e, accept, errc, stream);
-  else if (stride <= 256) launch_ascii_tma<E, 256>(reads, refs, (int)stride, ntiles, n, len, e, accept, errc, stream);
-  else if (stride <= 384) launch_ascii_tma<E, 384>(reads, refs, (int)stride, ntiles, n, len, e, accept, errc, stream);
-  else return 0;
-  return ntiles;
-}
-
 template <int E>
 static void launch_ascii_t(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n,
                            int len, int e, uint32_t* accept, uint8_t* errc, cudaStream_t stream) {
@@ -345,13 +177,8 @@ static void launch_ascii_t(const uint8_t* reads, const uint8_t* refs, int64_t st
 
 template <int E>
 void launch_ascii_all(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n,
-                             int len, int e, uint32_t* accept, uint8_t* errc,
-                             cudaStream_t stream) {
-  const int64_t done = try_ascii_tma<E>(reads, refs, stride, n, len, e, accept, errc, stream);
-  const int64_t p0 = done * 1024;  // remaining pairs: generic kernel on shifted pointers
-  if (p0 < n)
-    launch_ascii_t<E>(reads + p0 * stride, refs + p0 * stride, stride, n - p0, len, e,
-                      accept + p0 / 32, errc ? errc + p0 : nullptr, stream);
+                      int len, int e, uint32_t* accept, uint8_t* errc, cudaStream_t stream) {
+  launch_ascii_t<E>(reads, refs, stride, n, len, e, accept, errc, stream);
 }
 
 }  // namespace gk

@@ -27,6 +27,10 @@ int launch_filter_sweep(const uint32_t* reads, const uint32_t* refs, const uint3
 int launch_filter_ascii(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n,
                         int len, int e, uint32_t* accept, uint8_t* errc, cudaStream_t stream);
 
+// tile-per-CTA fused ASCII kernels (gk_fused.cu); false = cannot take the call
+bool launch_fused(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n, int len,
+                  int e, bool sweep, uint32_t* accept, uint8_t* errc, cudaStream_t stream);
+
 size_t compact_workspace_bytes(int64_t n, int rows = 1);
 // ibase is added to every written index (chunked host pipelines: absolute indices)
 int launch_compact(const uint32_t* bits, int64_t n, uint32_t* idx, uint64_t* n_acc, void* ws,

@@ -86,13 +86,15 @@ def run_workload(name: str, path: str | None = None, mem_gb: float = 60.0, max_p
         out = torch.zeros((rows, nch), dtype=torch.int64, device=dev)
         per_pair = 2 * b.L + b.L // 2 + 16 + rows * 2
         batch = max(HASH_CHUNK, int(mem_gb * 1e9 / per_pair) // HASH_CHUNK * HASH_CHUNK)
-        bpath = path or ("fused" if name == "c5" else "sweep")
+        from paper_2103_14978_b200.pipeline import auto_path
+        bpath = path or auto_path(b.L)
+        sweep = name != "c5"
         for s0 in range(0, n, batch):
             m = min(batch, n - s0)
             p_first = b.idx0 + s0
             reads, refs = pairgen.gen_pairs_cuda(m, b.L, idx0=p_first, device=dev)
-            if bpath == "sweep":
-                st = SweepStep(torch, m, b.L, b.emax, dev, compact_indices=False)
+            if sweep:
+                st = SweepStep(torch, m, b.L, b.emax, dev, compact_indices=False, path=bpath)
                 st.run(reads, refs, stream)
                 acc, err = st.accept[list(b.es)], st.errc[list(b.es)]
             else:
@@ -115,8 +117,8 @@ def run_workload(name: str, path: str | None = None, mem_gb: float = 60.0, max_p
             p0 = b.idx0 + c * HASH_CHUNK
             m = min(HASH_CHUNK, b.idx0 + n - p0)
             reads, refs = pairgen.gen_pairs_cuda(m, b.L, idx0=p0, device=dev)
-            if bpath == "sweep":
-                st = SweepStep(torch, m, b.L, b.emax, dev, compact_indices=False)
+            if sweep:
+                st = SweepStep(torch, m, b.L, b.emax, dev, compact_indices=False, path=bpath)
                 st.run(reads, refs, stream)
                 acc, err = st.accept[list(b.es)], st.errc[list(b.es)]
             else:

@@ -27,10 +27,9 @@ def test_full_size_parity(gk, name):
 
 
 @pytest.mark.parametrize("name,path", [("c2", "packed"), ("c2", "fused"), ("c3", "packed"),
-                                       ("c4", "packed"), ("c5", "packed")])
+                                       ("c3", "fused"), ("c5", "packed"), ("c5", "fused")])
 def test_slice_parity_other_paths(gk, name, path):
+    """Both the fused and the encode + filter paths on a 2M-pair slice of every bucket."""
     _golden_or_skip(name)
-    if name != "c5" and path in ("packed", "fused"):
-        pytest.skip("per-e paths of a sweep workload are covered by test_parity_gpu")
-    rec = full_parity.run_workload(name, path=path, max_pairs=1 << 20)
+    rec = full_parity.run_workload(name, path=path, max_pairs=2 << 20)
     assert rec["chunks_mismatching"] == 0, rec

@@ -594,3 +594,53 @@ def test_compute_sanitizer(gk, tool):
     out = p.stdout + p.stderr
     assert p.returncode == 0 and "sanitize_run ok" in out, out[-3000:]
     assert ("ERROR SUMMARY: 0 errors" in out or "(0 errors, 0 warnings)" in out), out[-3000:]
+
+
+# ------------------------------------------------------- fused ASCII sweep -----
+@pytest.mark.parametrize("n,L,emax", [(5000, 100, 10), (1024, 100, 6), (3073, 150, 15),
+                                      (2050, 64, 6), (1500, 33, 3), (2500, 250, 12),
+                                      (4100, 101, 10)])
+def test_filter_ascii_sweep(gk, n, L, emax):
+    """gk_filter_ascii_sweep (encode + one-pass sweep in one kernel, tiles in shared
+    memory): every row == the oracle's e-sweep, on balanced inputs with N, IUPAC and
+    lower case, full and partial tiles, odd lengths."""
+    reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, emax=emax,
+                                    seed=pairgen.SEED + n + L)
+    acc, err = gk.filter_ascii_sweep(to_dev(reads), to_dev(refs), emax)
+    torch.cuda.synchronize()
+    oa, oc = oracle.sweep_prefix(reads, refs, emax)
+    for e in range(emax + 1):
+        a = unpack_accept(acc[e], n)
+        c = err[e].cpu().numpy()[:n]
+        bad = np.nonzero((a != oa[e]) | (c != oc[e]))[0]
+        assert bad.size == 0, (e, bad[:5], a[bad[:5]], oa[e][bad[:5]], c[bad[:5]], oc[e][bad[:5]])
+
+
+@pytest.mark.parametrize("stride_pad", [0, 7, 28])
+def test_filter_ascii_fused_strides(gk, stride_pad):
+    """The fused kernels with row strides > len (TMA spans + the bounded staging of the
+    last tile, which must not read past (n-1)*stride+len) and both fused entry points."""
+    n, L, e = 3000, 100, 5
+    reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, emax=e,
+                                    stride=L + stride_pad)
+    # exact-size device buffers: the last row ends at (n-1)*stride + L
+    flat_r = torch.from_numpy(reads.reshape(-1)[: (n - 1) * (L + stride_pad) + L].copy()).cuda()
+    flat_f = torch.from_numpy(refs.reshape(-1)[: (n - 1) * (L + stride_pad) + L].copy()).cuda()
+    lib = gk.load_library()
+    acc = torch.empty(gk.result_words(n), dtype=torch.int32, device="cuda")
+    err = torch.empty(n, dtype=torch.uint8, device="cuda")
+    rc = lib.gk_filter_ascii(flat_r.data_ptr(), flat_f.data_ptr(), L + stride_pad, n, L, e,
+                             acc.data_ptr(), err.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    acc2 = torch.empty((e + 1, gk.result_words(n)), dtype=torch.int32, device="cuda")
+    err2 = torch.empty((e + 1, n), dtype=torch.uint8, device="cuda")
+    rc = lib.gk_filter_ascii_sweep(flat_r.data_ptr(), flat_f.data_ptr(), L + stride_pad, n, L, e,
+                                   acc2.data_ptr(), err2.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    oa, oc = oracle.sweep_prefix(reads, refs, e, L=L)
+    assert (unpack_accept(acc, n) == oa[e]).all() and (err.cpu().numpy() == oc[e]).all()
+    for k in range(e + 1):
+        assert (unpack_accept(acc2[k], n) == oa[k]).all(), k
+        assert (err2[k].cpu().numpy() == oc[k]).all(), k

@@ -44,11 +44,23 @@ def main():
     res = {"lib": a.tag}
     for L in a.L:
         r, f = pairgen.gen_pairs_cuda(a.n, L)
-        q, uq = gk.encode(r, L)
-        s, us = gk.encode(f, L)
-        del r, f
         e5 = L // 20
         emax = (L + 9) // 10
+        q, uq = gk.encode(r, L)
+        s, us = gk.encode(f, L)
+        res[f"{L}bp_encode_x2_ms"] = round(timed(lambda: (gk.encode(r, L, out=(q, uq)),
+                                                          gk.encode(f, L, out=(s, us)))), 4)
+        accf, errf = gk.filter_ascii(r, f, e5)
+        res[f"{L}bp_fused_e{e5}_ms"] = round(timed(lambda: gk.filter_ascii(
+            r, f, e5, accept=accf, errcount=errf)), 4)
+        try:
+            accs, errs = gk.filter_ascii_sweep(r, f, emax)
+            res[f"{L}bp_fused_sweep_e0-{emax}_ms"] = round(timed(lambda: gk.filter_ascii_sweep(
+                r, f, emax, accept=accs, errcount=errs)), 4)
+            del accs, errs
+        except gk.GateKeeperError as ex:
+            res[f"{L}bp_fused_sweep_e0-{emax}_ms"] = str(ex)
+        del r, f, accf, errf
         acc, err = gk.filter(q, s, uq, us, a.n, L, e5)
         res[f"{L}bp_filter_e{e5}_ms"] = round(timed(lambda: gk.filter(q, s, uq, us, a.n, L, e5,
                                                                        accept=acc, errcount=err)), 4)
