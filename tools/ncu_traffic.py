@@ -10,7 +10,7 @@ import subprocess
 
 p = argparse.ArgumentParser()
 p.add_argument("report")
-p.add_argument("--workload", required=True, help="config:path:n_pairs the capture ran")
+p.add_argument("--workload", required=True, help="config:path the capture ran (bench.py's key)")
 a = p.parse_args()
 out = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
@@ -31,14 +31,22 @@ for r in rows[2:]:
     rd = val(r, "dram__bytes_read.sum", scale)
     wr = val(r, "dram__bytes_write.sum", scale)
     ms = val(r, "gpu__time_duration.sum", tscale)
-    kernels.setdefault(name, []).append({"dram_read_bytes": rd, "dram_write_bytes": wr,
-                                         "traffic_bytes": rd + wr, "ms": ms})
+    ent = {"dram_read_bytes": rd, "dram_write_bytes": wr, "traffic_bytes": rd + wr, "ms": ms}
+    for key, col in (("pipe_alu_pct", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                     ("pipe_fma_pct", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                     ("issue_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                     ("warp_inst", "smsp__inst_executed.sum")):
+        if col in hdr:
+            ent[key] = float(r[hdr.index(col)].replace(",", ""))
+    kernels.setdefault(name, []).append(ent)
 res = {"workload": a.workload, "source": a.report.split("/")[-1],
        "method": "ncu --set full --clock-control none, one capture per launch",
        "kernels": {k: {"launches": len(v),
                        "traffic_bytes_per_launch": sum(x["traffic_bytes"] for x in v) / len(v),
                        "dram_read_bytes_per_launch": sum(x["dram_read_bytes"] for x in v) / len(v),
                        "dram_write_bytes_per_launch": sum(x["dram_write_bytes"] for x in v) / len(v),
-                       "ms_per_launch_under_ncu": sum(x["ms"] for x in v) / len(v)}
+                       "ms_per_launch_under_ncu": sum(x["ms"] for x in v) / len(v),
+                       **{k: sum(x[k] for x in v) / len(v) for k in
+                          ("pipe_alu_pct", "pipe_fma_pct", "issue_pct", "warp_inst") if k in v[0]}}
                    for k, v in kernels.items()}}
 print(json.dumps(res, indent=1))
