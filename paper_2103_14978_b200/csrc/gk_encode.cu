@@ -18,6 +18,10 @@
 #include "gk_kernels.cuh"
 #include "gk_tma.cuh"
 
+// minimum resident CTAs per SM asked of ptxas for encode3_kernel (A/B knob)
+#ifndef GK_ENC3_MINB
+#define GK_ENC3_MINB 0  // 0: per length class (launch_enc3_t)
+#endif
 #ifndef GK_ENCODE_TMA
 #define GK_ENCODE_TMA 1
 #endif
@@ -212,7 +216,11 @@ template <int NCH, bool ALN>
 static void launch_enc3_t(const uint8_t* seqs, int64_t nblocks, int len, int stride,
                           uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
   const Enc3Cfg c = enc3_cfg(len, stride);
-  auto kern = encode3_kernel<NCH, ALN, 1>;
+  // registers vs resident CTAs, measured per length class (profiles/r02_ab_encoder_minb.jsonl):
+  // 100 bp 8 CTAs/SM (64 regs, 1.51 -> 1.39 ms per 2 x 30M), 150 bp 5 (2.40 -> 2.31 ms),
+  // 250 bp unbounded (shared memory limits it to 3 anyway; bounded was slower)
+  constexpr int MB = GK_ENC3_MINB > 0 ? GK_ENC3_MINB : (NCH == 7 ? 8 : (NCH == 10 ? 5 : 1));
+  auto kern = encode3_kernel<NCH, ALN, MB>;
   // launch configuration cached per (device, smem): the attribute and occupancy
   // queries are host round trips, kept off the per-call path
   static thread_local int cached_dev = -1, cached_grid = 0;

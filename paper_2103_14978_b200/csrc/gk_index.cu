@@ -8,12 +8,11 @@
 // the same way (row r at bits [r*L, r*L+L)), so a read with many candidates is
 // encoded once.
 //
-// gather: one CTA per tile, one warp per group of 32 pairs (lane j = pair j).  For each chunk of
-// 32 positions lane j funnel-shifts its window bits out of two plane words
-// (any bit offset), then a 5-stage shuffle transpose of the 32x32 bit matrix
-// turns "32 positions of pair j" into "position i of 32 pairs" -- the
-// bit-sliced packed layout of gk_encode (include/gatekeeper.h), which
-// gk_filter / gk_filter_sweep consume unchanged.
+// gather (gather2_kernel below): lane j = pair j funnel-shifts its window bits
+// out of the plane blocks (any bit offset), then a 5-stage shuffle transpose of
+// the 32x32 bit matrix turns "32 positions of pair j" into "position i of 32
+// pairs" -- the bit-sliced packed layout of gk_encode (include/gatekeeper.h),
+// which gk_filter / gk_filter_sweep consume unchanged.
 #include "gk_common.cuh"
 #include "gk_kernels.cuh"
 
@@ -49,81 +48,6 @@ __global__ void pack_planes_kernel(const uint8_t* __restrict__ rows, int64_t n_r
   }
 }
 
-// ---- gather: windows -> bit-sliced packed words --------------------------------
-// 32x32 bit transpose across a warp: on entry lane j holds x (bit i = element
-// (j, i)); on exit lane i holds bit j = element (j, i).
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
-  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-  for (int t = 0; t < 5; ++t) {
-    const int s = 16 >> t;
-    const uint32_t m = masks[t];
-    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
-    // lanes with bit s clear keep their low halves (bit blocks of size s) and take
-    // the partner's low halves into their high halves; lanes with bit s set the
-    // converse
-    x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
-  }
-  return x;
-}
-
-// Bits [bit, bit+32) of the three planes: two 16-byte loads (the planes of a
-// 32-base block are interleaved, so a random window touches 2-3 sectors, not 6).
-__device__ __forceinline__ void window_bits(const uint4* __restrict__ p, int64_t bit, uint32_t& h,
-                                            uint32_t& l, uint32_t& b) {
-  const int64_t w = bit >> 5;
-  const uint32_t sh = (uint32_t)(bit & 31);
-  const uint4 a = __ldg(p + w), c = __ldg(p + w + 1);
-  h = __funnelshift_r(a.x, c.x, sh);
-  l = __funnelshift_r(a.y, c.y, sh);
-  b = __funnelshift_r(a.z, c.z, sh);
-}
-
-// One CTA of 32 warps per tile of 1024 pairs (warp = group of 32 pairs, lane =
-// pair).  Per chunk of 32 positions each warp transposes its words into a
-// shared [32 positions][32 groups] staging tile, so the tile's chunk -- 32 x
-// 256 contiguous bytes of the packed layout -- leaves in full, coalesced lines
-// (a warp alone would write 8-byte pieces at a 256-byte stride).
-__global__ void __launch_bounds__(1024) gather_windows_kernel(
-    const uint4* __restrict__ planes, int64_t nbases, const int64_t* __restrict__ offsets,
-    int64_t n, int len, uint32_t* __restrict__ packed, uint32_t* __restrict__ undef) {
-  __shared__ uint2 stage[32][32];  // [position in chunk][group in tile]
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int64_t tile = blockIdx.x;
-  const int64_t g = tile * 32 + warp;
-  const int64_t p = g * 32 + lane;
-  int64_t off = p < n ? offsets[p] : -1;
-  // a window outside [0, nbases) makes the pair undefined (accepted, 255)
-  const bool oob = p < n && (off < 0 || off + len > nbases);
-  const bool live = p < n && !oob;
-  if (!live) off = 0;
-  uint32_t anybad = 0u;
-  uint4* dst = reinterpret_cast<uint4*>(packed + tile * (int64_t)len * 64);
-  for (int c0 = 0; c0 < len; c0 += 32) {
-    const int nb = len - c0 < 32 ? len - c0 : 32;
-    const uint32_t vm = nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u);
-    uint32_t xh = 0u, xl = 0u;
-    if (live) {
-      uint32_t xb;
-      window_bits(planes, off + c0, xh, xl, xb);
-      xh &= vm;
-      xl &= vm;
-      anybad |= xb & vm;
-    }
-    const uint32_t yh = warp_transpose32(xh, lane);
-    const uint32_t yl = warp_transpose32(xl, lane);
-    stage[lane][warp] = make_uint2(yh, yl);
-    __syncthreads();
-    // nb positions x 256 bytes = nb * 16 uint4, contiguous from position c0
-    const uint4* src = reinterpret_cast<const uint4*>(&stage[0][0]);
-    for (int t = threadIdx.x; t < nb * 16; t += 1024) dst[(int64_t)c0 * 16 + t] = src[t];
-    __syncthreads();
-  }
-  const uint32_t u = __ballot_sync(0xFFFFFFFFu, anybad != 0u || oob);
-  if (lane == 0) undef[g] = u;
-}
-
 int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int len, int64_t stride,
                        uint32_t* planes, cudaStream_t stream) {
   const int64_t total = n_rows * (int64_t)len;
@@ -136,12 +60,99 @@ int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int len, int64_t str
   return 0;
 }
 
+// ---- gather v2 --------------------------------------------------------------
+// CTA = 4 warps = 4 consecutive groups (128 pairs), lane = pair.  Every lane
+// issues the loads of its whole window up front (NCH+1 16-byte plane blocks:
+// bits [off, off+32*NCH) are funnel shifts of consecutive blocks), then per
+// 32-position chunk transposes its two plane words with a 5-stage shuffle
+// transpose (rotate + select per stage: SHFL + SHF + LOP3) into a small
+// [positions][4 groups] staging tile that leaves as full 32-byte sectors
+// (4 groups x 8 bytes per position, as gk_encode's output).  One barrier per
+// CTA; 3 KB of shared memory at 100 bp, so many CTAs per SM keep enough random
+// window loads in flight (round 1: one 1024-thread CTA per tile, two barriers
+// per chunk and two dependent loads per chunk: 25% of HBM).
+struct T32 {
+  uint32_t keep[5], rot[5];
+  __device__ __forceinline__ void init(int lane) {
+    const uint32_t Z[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+      const int s = 16 >> t;
+      const bool up = (lane & s) != 0;
+      keep[t] = up ? ~Z[t] : Z[t];
+      rot[t] = up ? (uint32_t)(32 - s) : (uint32_t)s;
+    }
+  }
+  // lane j holds bit i = element (j, i) -> lane i holds bit j = element (j, i)
+  __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+      const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, 16 >> t);
+      const uint32_t r = __funnelshift_l(y, y, rot[t]);
+      x = (x & keep[t]) | (r & ~keep[t]);
+    }
+    return x;
+  }
+};
+
+template <int NCH>
+__global__ void __launch_bounds__(128) gather2_kernel(
+    const uint4* __restrict__ planes, int64_t nbases, const int64_t* __restrict__ offsets,
+    int64_t n, int len, uint32_t* __restrict__ packed, uint32_t* __restrict__ undef) {
+  extern __shared__ uint2 stage2[];  // [len][4]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t g = (int64_t)blockIdx.x * 4 + warp;
+  const int64_t p = g * 32 + lane;
+  int64_t off = p < n ? offsets[p] : -1;
+  const bool oob = p < n && (off < 0 || off + len > nbases);
+  const bool live = p < n && !oob;
+  if (!live) off = 0;
+  const int nch = (len + 31) >> 5;
+  const int64_t w0 = off >> 5;
+  const uint32_t sh = (uint32_t)(off & 31);
+  uint4 blk[NCH + 1];
+#pragma unroll
+  for (int c = 0; c <= NCH; ++c)
+    blk[c] = (live && c <= nch) ? __ldg(planes + w0 + c) : make_uint4(0u, 0u, 0u, 0u);
+  T32 tr;
+  tr.init(lane);
+  uint32_t anybad = 0u;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (c < nch) {
+      const int nb = len - 32 * c < 32 ? len - 32 * c : 32;
+      const uint32_t vm = nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u);
+      const uint32_t xh = __funnelshift_r(blk[c].x, blk[c + 1].x, sh) & vm;
+      const uint32_t xl = __funnelshift_r(blk[c].y, blk[c + 1].y, sh) & vm;
+      anybad |= __funnelshift_r(blk[c].z, blk[c + 1].z, sh) & vm;
+      const uint32_t yh = tr(xh), yl = tr(xl);
+      if (lane < nb) stage2[(32 * c + lane) * 4 + warp] = make_uint2(yh, yl);
+    }
+  }
+  const uint32_t u = __ballot_sync(0xFFFFFFFFu, anybad != 0u || oob);
+  if (lane == 0) undef[g] = u;
+  __syncthreads();
+  // 4 groups x 8 bytes per position: one 32-byte sector each
+  const int64_t tile = (g - warp) >> 5;
+  const int gl0 = (int)((g - warp) & 31);
+  uint2* dst = reinterpret_cast<uint2*>(packed);
+  for (int t = threadIdx.x; t < 4 * len; t += 128)
+    dst[(tile * len + (t >> 2)) * 32 + gl0 + (t & 3)] = stage2[t];
+}
+
 int launch_gather_windows(const uint32_t* planes, int64_t nbases, const int64_t* offsets, int64_t n,
                           int len, uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
   const int64_t tiles = (n + 1023) / 1024;  // whole tiles (zero-filled tail)
+  const int64_t ctas = tiles * 8;
+  const size_t smem = (size_t)len * 4 * 8;
+  const uint4* pl = reinterpret_cast<const uint4*>(planes);
   count_launch();
-  gather_windows_kernel<<<(unsigned)tiles, 1024, 0, stream>>>(
-      reinterpret_cast<const uint4*>(planes), nbases, offsets, n, len, packed, undef);
+  if (len <= 128)
+    gather2_kernel<4><<<(unsigned)ctas, 128, smem, stream>>>(pl, nbases, offsets, n, len, packed, undef);
+  else if (len <= 256)
+    gather2_kernel<8><<<(unsigned)ctas, 128, smem, stream>>>(pl, nbases, offsets, n, len, packed, undef);
+  else
+    gather2_kernel<16><<<(unsigned)ctas, 128, smem, stream>>>(pl, nbases, offsets, n, len, packed, undef);
   return 0;
 }
 
