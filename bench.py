@@ -226,23 +226,23 @@ def int_peak():
 
 
 def load_ncu(workload):
-    """Per-launch DRAM traffic and ALU-pipe utilisation of this workload's kernels from
-    the newest committed ncu --set full capture (profiles/r*_traffic.json)."""
+    """Per-launch DRAM traffic and pipe utilisation of this workload's kernels from the
+    committed ncu --set full captures (profiles/r*_traffic.json, written by
+    tools/ncu_traffic.py; one capture per kernel, newest file wins per kernel)."""
     import glob
-    best = None
+    best = {}
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json"))):
         try:
             with open(path) as f:
                 d = json.load(f)
         except (OSError, ValueError):
             continue
-        if d.get("workload") == workload:
-            best = {}
-            for k, v in d.get("kernels", {}).items():
-                name = k.split("(")[0].strip()
-                best[name] = v
-                best.setdefault(name.split("<")[0].strip(), v)
-    return best
+        if d.get("workload") != workload:
+            continue
+        for k, v in d.get("kernels", {}).items():
+            name = k.split("(")[0].replace("void ", "").strip()
+            best[name] = dict(v, source=os.path.basename(path), kernel=name)
+    return best or None
 
 
 def cpu_model():
@@ -576,6 +576,8 @@ def run_buckets(args, ctx):
 
     # roofline of every kernel family; the dominant one is the largest share of the step
     ncu = load_ncu(f"{args.config}:{args.path}")  # profiles/r*_traffic.json of this workload
+    if ncu is None and args.path == "auto":
+        ncu = load_ncu(f"{args.config}:auto")
     kernels = []
     for kname, kms in kern_ms.items():
         b, o, parts = kern_work[kname]
@@ -593,9 +595,19 @@ def run_buckets(args, ctx):
                "per_launch_group": parts,
                "peak_source": alu_src if bound == "alu" else peak_src}
         if ncu:
-            hit = [v for k, v in ncu.items() if kname in k]
+            fam = {"encode": "encode3", "filter": "filter_", "compact": "compact_write",
+                   "compact_rows": "compact_write", "filter_sweep": "filter_bt2_sweep",
+                   "filter_ascii": "fused_kernel", "filter_ascii_sweep": "fused_kernel"}[kname]
+            hit = [v for k, v in sorted(ncu.items()) if fam in k and
+                   (kname != "filter" or "sweep" not in k)]
             if hit:
                 ent["traffic"] = hit[0].get("traffic_bytes_per_launch")
+                ent["traffic_kernel"] = hit[0]["kernel"]
+                ent["traffic_source"] = hit[0]["source"]
+                ent["ncu_per_instantiation"] = [
+                    {k2: h[k2] for k2 in ("kernel", "traffic_bytes_per_launch", "pipe_alu_pct",
+                                          "pipe_fma_pct", "issue_pct", "source") if k2 in h}
+                    for h in hit]
                 if "pipe_alu_pct" in hit[0]:
                     ent["ncu_pipe_alu_pct"] = hit[0]["pipe_alu_pct"]
         ent.setdefault("traffic", None)

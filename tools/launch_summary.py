@@ -18,12 +18,13 @@ def main(path, cmd):
         name = r[ki].split("(")[0]
         agg[name][0] += 1
         agg[name][1] += float(r[vi].replace(",", "")) * SCALE[r[ui]]
-    untimed = ("pg_gen", "at::", "edit_distance", "accuracy_kernel")
+    untimed = ("pg_gen", "at::", "edit_distance", "accuracy_kernel", "peak_kernel")
     tot = sum(t for k, (c, t) in agg.items() if not any(u in k for u in untimed))
     print("ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised) of")
     print(f"  {cmd}")
-    print("shares exclude the input generator (pg_gen_kernel, untimed setup), torch fills and the")
-    print("accuracy harness (edit_distance / accuracy kernels, run after the timed region)")
+    print("shares exclude the input generator (pg_gen_kernel, untimed setup), torch fills, the")
+    print("accuracy harness (edit_distance / accuracy kernels, run after the timed region) and the")
+    print("integer-peak microbenchmark (peak_kernel, run before it)")
     print(f"{'kernel':48s} {'launches':>8s} {'total_us':>12s} {'us/launch':>10s} {'share':>7s}")
     for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         share = f"{t / tot:7.3f}" if not any(u in k for u in untimed) else "      -"
