@@ -31,10 +31,13 @@ namespace gk {
 
 
 #ifndef GK_BT2_B
-#define GK_BT2_B 8
+#define GK_BT2_B 8      // positions per block of the sweep kernel
+#endif
+#ifndef GK_BT2_B_E
+#define GK_BT2_B_E 16   // positions per block of the per-e kernel (2 CTAs/SM, 252 regs)
 #endif
 #ifndef GK_BT2_MINB
-#define GK_BT2_MINB 3
+#define GK_BT2_MINB 2
 #endif
 #ifndef GK_BT2_SWEEP_MINB
 #define GK_BT2_SWEEP_MINB 6
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(BT2_SWEEP_WARPS * 32, GK_BT2_SWEEP_MINB) filte
 void launch_bt2(const uint2* reads, const uint2* refs, const uint32_t* rund, const uint32_t* fund,
                 int64_t n, int len, int e, uint32_t* accept, uint8_t* errc, int edge_fix,
                 cudaStream_t stream) {
-  constexpr int B = GK_BT2_B;
+  constexpr int B = GK_BT2_B_E;
   const int64_t tiles = (n + 1023) / 1024;
   const int warps = 4;
   const int64_t blocks = (tiles + warps - 1) / warps;
