@@ -651,7 +651,9 @@ def measure_e2e(args, ctx, bk):
     t_step, h2d, d2h, desc = 0.0, 0, 0, []
     for L, es, idx0, n in bk:
         lo, cnt = sharding.even_shard(n, rank, world) if c5 else sharding.weak_shard(n, rank)
-        ns = min(cnt, 1 << 23)
+        # pinned host sample per rank (8M pairs per bucket at N=1, less per rank at N>1
+        # so that N ranks of one node do not pin N x 8 GB)
+        ns = min(cnt, max(1 << 20, ((1 << 23) // world) // 1024 * 1024))
         r_d, f_d = pairgen.gen_pairs_cuda(ns, L, idx0=idx0 + lo, device=dev)
         hr = torch.empty((ns, L), dtype=torch.uint8, pin_memory=True)
         hf = torch.empty((ns, L), dtype=torch.uint8, pin_memory=True)

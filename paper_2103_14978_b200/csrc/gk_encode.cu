@@ -19,6 +19,10 @@
 #include "gk_tma.cuh"
 
 // minimum resident CTAs per SM asked of ptxas for encode3_kernel (A/B knob)
+// span buffers per warp (A/B knob): 2 = double-buffered, 1 = more CTAs per SM
+#ifndef GK_ENC3_NBUF
+#define GK_ENC3_NBUF 0  // 0: per length class (launch_enc3_t)
+#endif
 #ifndef GK_ENC3_MINB
 #define GK_ENC3_MINB 0  // 0: per length class (launch_enc3_t)
 #endif
@@ -121,7 +125,44 @@ __device__ __forceinline__ void enc3_chunk(const uint8_t* buf, const uint32_t (&
   if (!tail || pos < len) outs[plane * P + pos * 5 + wg] = m;
 }
 
-template <int NCH, bool ALN, int MB>
+// stride = 2 (mod 4): the rows of a lane all start at the same 2-byte offset
+// (its rows have one parity), so every lane loads ONE aligned word per row (not
+// two + a funnel shift: half the shared-memory loads) and a lane whose rows start
+// 2 bytes into a word realigns its MERGED word instead: in the merged layout
+// (bit = b' + 2i + 8k) a 2-position shift is a 16-bit funnel shift with the
+// merged word of the next column (lane + 1, or for column 3 lane - 3 of the next
+// chunk) -- one SHFL + one SHF per 16 positions.  Chunks are therefore emitted
+// one step late, with one extra load chunk at the end.
+__device__ __forceinline__ uint32_t enc3_merge_m2(const uint8_t* buf, const uint32_t (&roff)[4],
+                                                  int s2, int c, int len, const enc3::Lane& ln,
+                                                  uint32_t (&ag)[4], uint32_t (&ay)[4],
+                                                  bool first, bool tail) {
+  uint32_t x[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t w = *reinterpret_cast<const uint32_t*>(buf + roff[i] + 16 * c);
+    uint32_t bm = 0xFFFFFFFFu;
+    if (first && s2 && ln.cw == 0) bm = 0xFFFF0000u;  // the 2 bytes before the row start
+    if (tail) {
+      const int rem = len - (16 * c + 4 * ln.cw - s2);  // bytes of positions < len
+      bm &= rem >= 4 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * rem)));
+    }
+    if (first || tail) w = (w & bm) | (0x41414141u & ~bm);
+    x[i] = enc3::row_word(w, ln, ag[i], ay[i]);
+  }
+  return enc3::merge4(x[0], x[1], x[2], x[3], ln);
+}
+
+__device__ __forceinline__ void enc3_emit(uint32_t m, int c, int len, const enc3::Lane& ln,
+                                          uint32_t* outs, uint32_t P, int wg) {
+  m = enc3::transpose3(m, ln);
+  const int lane = threadIdx.x & 31;
+  const int pos = 16 * c + 4 * (lane & 3) + (lane >> 3);
+  const int plane = ((lane >> 2) & 1) ? 0 : 1;
+  if (pos < len) outs[plane * P + pos * 5 + wg] = m;
+}
+
+template <int NCH, int MODE, int MB, int NB>
 __global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restrict__ seqs,
                                                          int64_t nblocks, int len, int stride,
                                                          uint32_t bufb, uint32_t P,
@@ -129,8 +170,8 @@ __global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restr
                                                          uint32_t* __restrict__ undef) {
   extern __shared__ __align__(128) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* stage = sm + (size_t)warp * 2 * bufb;                               // [2][bufb]
-  uint32_t* outs = reinterpret_cast<uint32_t*>(sm + (size_t)4 * 2 * bufb);     // [2][P]
+  uint8_t* stage = sm + (size_t)warp * NB * bufb;                              // [NB][bufb]
+  uint32_t* outs = reinterpret_cast<uint32_t*>(sm + (size_t)4 * NB * bufb);    // [2][P]
   uint64_t* bars = reinterpret_cast<uint64_t*>(outs + 2 * P);
   uint64_t* mybar = bars + 2 * warp;
   if (lane == 0) {
@@ -145,9 +186,10 @@ __global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restr
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint32_t a = (uint32_t)ln.rows[i] * (uint32_t)stride + 4u * (uint32_t)ln.cw;
-    roff[i] = ALN ? a : (a & ~3u);
+    roff[i] = MODE == 0 ? a : (a & ~3u);
     rsh[i] = (a & 3u) * 8u;
   }
+  const int s2 = (int)(rsh[0] >> 3);  // MODE 2: the lane's rows start 0 or 2 bytes into a word
   const uint32_t span = 32u * (uint32_t)stride;
   const int nch = NCH > 0 ? NCH : (len + 15) >> 4;
 
@@ -158,32 +200,54 @@ __global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restr
     tma_load_1d(stage, seqs + (4 * b + warp) * (int64_t)span, span, &mybar[0]);
   }
   for (int it = 0; b < nblocks; ++it, b += gridDim.x) {
-    const int buf = it & 1;
+    const int buf = NB == 2 ? (it & 1) : 0;
     const int64_t bn = b + gridDim.x;
-    if (lane == 0 && bn < nblocks) {
+    if (NB == 2 && lane == 0 && bn < nblocks) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&mybar[buf ^ 1], span);
       tma_load_1d(stage + (buf ^ 1) * bufb, seqs + (4 * bn + warp) * (int64_t)span, span,
                   &mybar[buf ^ 1]);
     }
-    mbar_wait(&mybar[buf], (uint32_t)(it >> 1) & 1u);
+    mbar_wait(&mybar[buf], NB == 2 ? ((uint32_t)(it >> 1) & 1u) : ((uint32_t)it & 1u));
     const uint8_t* sbuf = stage + buf * bufb;
     // one output staging buffer (smem for more CTAs per SM): the previous block's
     // copy-out must be complete before it is overwritten
     if (it > 0) __syncthreads();
     uint32_t ag[4] = {0u, 0u, 0u, 0u}, ay[4] = {0u, 0u, 0u, 0u};
-    if (NCH > 0) {
-#pragma unroll
-      for (int c = 0; c < (NCH > 1 ? NCH - 1 : 0); ++c)
-        enc3_chunk<ALN>(sbuf, roff, rsh, c, len, ln, ag, ay, outs, P, warp, false);
+    if constexpr (MODE == 2) {
+      const int cw = ln.cw;
+      const int src = cw == 3 ? lane - 3 : lane + 1;
+      uint32_t prev = enc3_merge_m2(sbuf, roff, s2, 0, len, ln, ag, ay, true, nch <= 1);
+#pragma unroll (NCH > 0 ? NCH : 1)
+      for (int c = 1; c <= nch; ++c) {
+        const uint32_t cur = enc3_merge_m2(sbuf, roff, s2, c, len, ln, ag, ay, false, c >= nch - 1);
+        const uint32_t nxt = __shfl_sync(0xFFFFFFFFu, cw == 0 ? cur : prev, src);
+        enc3_emit(__funnelshift_r(prev, nxt, (uint32_t)(8 * s2)), c - 1, len, ln, outs, P, warp);
+        prev = cur;
+      }
     } else {
+      constexpr bool ALN = MODE == 0;
+      if (NCH > 0) {
+#pragma unroll
+        for (int c = 0; c < (NCH > 1 ? NCH - 1 : 0); ++c)
+          enc3_chunk<ALN>(sbuf, roff, rsh, c, len, ln, ag, ay, outs, P, warp, false);
+      } else {
 #pragma unroll 1
-      for (int c = 0; c < nch - 1; ++c)
-        enc3_chunk<ALN>(sbuf, roff, rsh, c, len, ln, ag, ay, outs, P, warp, false);
+        for (int c = 0; c < nch - 1; ++c)
+          enc3_chunk<ALN>(sbuf, roff, rsh, c, len, ln, ag, ay, outs, P, warp, false);
+      }
+      enc3_chunk<ALN>(sbuf, roff, rsh, nch - 1, len, ln, ag, ay, outs, P, warp, true);
     }
-    enc3_chunk<ALN>(sbuf, roff, rsh, nch - 1, len, ln, ag, ay, outs, P, warp, true);
     const uint32_t und = enc3::group_undef(ag, ay, ln);
     if (lane == 0) undef[4 * b + warp] = und;
+    if (NB == 1) {  // single buffer: the next span lands during the copy-out below
+      __syncwarp();
+      if (lane == 0 && bn < nblocks) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&mybar[0], span);
+        tma_load_1d(stage, seqs + (4 * bn + warp) * (int64_t)span, span, &mybar[0]);
+      }
+    }
     __syncthreads();
     // write the 4 groups' words: per position 32 contiguous bytes
     const int64_t tile = (4 * b) >> 5;
@@ -202,25 +266,27 @@ struct Enc3Cfg {
   size_t smem;
 };
 
-static Enc3Cfg enc3_cfg(int len, int stride) {
+static Enc3Cfg enc3_cfg(int len, int stride, int nbuf) {
   Enc3Cfg c;
   c.bufb = ((uint32_t)(32 * stride + 32) + 127u) & ~127u;
   uint32_t p = (uint32_t)(5 * len);
   p = (p + 31u) & ~31u;
   c.P = p + 16u;  // P = 16 (mod 32): the two planes' transposed writes hit disjoint banks
-  c.smem = (size_t)4 * 2 * c.bufb + (size_t)2 * c.P * 4 + 8 * 8;
+  c.smem = (size_t)4 * nbuf * c.bufb + (size_t)2 * c.P * 4 + 8 * 8;
   return c;
 }
 
-template <int NCH, bool ALN>
+template <int NCH, int MODE>
 static void launch_enc3_t(const uint8_t* seqs, int64_t nblocks, int len, int stride,
                           uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
-  const Enc3Cfg c = enc3_cfg(len, stride);
-  // registers vs resident CTAs, measured per length class (profiles/r02_ab_encoder_minb.jsonl):
-  // 100 bp 8 CTAs/SM (64 regs, 1.51 -> 1.39 ms per 2 x 30M), 150 bp 5 (2.40 -> 2.31 ms),
-  // 250 bp unbounded (shared memory limits it to 3 anyway; bounded was slower)
-  constexpr int MB = GK_ENC3_MINB > 0 ? GK_ENC3_MINB : (NCH == 7 ? 8 : (NCH == 10 ? 5 : 1));
-  auto kern = encode3_kernel<NCH, ALN, MB>;
+  // registers vs resident CTAs and span buffers per warp, measured per length class
+  // (profiles/r02_ab_encoder_minb.jsonl, r02_ab_encoder_nbuf.jsonl): 100 bp double-
+  // buffered at 8 CTAs/SM (64 regs; 1.51 -> 1.39 ms per 2 x 30M); 150 bp single-
+  // buffered at 6 (2.40 -> 2.28 ms); 250 bp single-buffered at 5 (3.95 -> 3.51 ms)
+  constexpr int MB = GK_ENC3_MINB > 0 ? GK_ENC3_MINB : (NCH == 7 ? 8 : (NCH == 10 ? 6 : (NCH == 16 ? 5 : 1)));
+  constexpr int NB = GK_ENC3_NBUF > 0 ? GK_ENC3_NBUF : (NCH == 7 || NCH == 0 ? 2 : 1);
+  const Enc3Cfg c = enc3_cfg(len, stride, NB);
+  auto kern = encode3_kernel<NCH, MODE, MB, NB>;
   // launch configuration cached per (device, smem): the attribute and occupancy
   // queries are host round trips, kept off the per-call path
   static thread_local int cached_dev = -1, cached_grid = 0;
@@ -247,19 +313,23 @@ static void launch_enc3_t(const uint8_t* seqs, int64_t nblocks, int len, int str
 static void launch_enc3(const uint8_t* seqs, int64_t nblocks, int len, int stride,
                         uint32_t* packed, uint32_t* undef, cudaStream_t stream) {
   const int nch = (len + 15) >> 4;
-  const bool aln = (stride & 3) == 0;
-#define GK_ENC3(N)                                                                      \
-  if (nch == N) {                                                                       \
-    if (aln) launch_enc3_t<N, true>(seqs, nblocks, len, stride, packed, undef, stream); \
-    else launch_enc3_t<N, false>(seqs, nblocks, len, stride, packed, undef, stream);    \
-    return;                                                                             \
+  // MODE 0: rows 4-byte aligned; 2: stride = 2 (mod 4) (one load per word + merged-word
+  // realignment); 1: any other stride (two loads + funnel shift per word)
+  const int mode = (stride & 3) == 0 ? 0 : ((stride & 3) == 2 ? 2 : 1);
+#define GK_ENC3(N)                                                                        \
+  if (nch == N) {                                                                         \
+    if (mode == 0) launch_enc3_t<N, 0>(seqs, nblocks, len, stride, packed, undef, stream); \
+    else if (mode == 2) launch_enc3_t<N, 2>(seqs, nblocks, len, stride, packed, undef, stream); \
+    else launch_enc3_t<N, 1>(seqs, nblocks, len, stride, packed, undef, stream);          \
+    return;                                                                               \
   }
   GK_ENC3(7)   // 97..112 bp (100 bp)
   GK_ENC3(10)  // 145..160 bp (150 bp)
   GK_ENC3(16)  // 241..256 bp (250 bp)
 #undef GK_ENC3
-  if (aln) launch_enc3_t<0, true>(seqs, nblocks, len, stride, packed, undef, stream);
-  else launch_enc3_t<0, false>(seqs, nblocks, len, stride, packed, undef, stream);
+  if (mode == 0) launch_enc3_t<0, 0>(seqs, nblocks, len, stride, packed, undef, stream);
+  else if (mode == 2) launch_enc3_t<0, 2>(seqs, nblocks, len, stride, packed, undef, stream);
+  else launch_enc3_t<0, 1>(seqs, nblocks, len, stride, packed, undef, stream);
 }
 
 static void launch_generic(const uint8_t* seqs, int64_t n, int len, int64_t stride,

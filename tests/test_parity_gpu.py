@@ -64,7 +64,12 @@ def assert_parity(gk, reads, refs, e, L=None, flags=0, path="packed"):
 @pytest.mark.parametrize("L,n,stride,offset", [
     (100, 3000, 100, 0), (1, 40, 1, 0), (2, 33, 2, 0), (3, 1025, 5, 0), (31, 100, 31, 1),
     (32, 2048, 32, 0), (33, 999, 40, 3), (150, 1500, 150, 0), (150, 700, 160, 7),
-    (250, 2100, 256, 0), (508, 300, 508, 0), (508, 64, 1024, 5), (17, 5000, 17, 2)])
+    (250, 2100, 256, 0), (508, 300, 508, 0), (508, 64, 1024, 5), (17, 5000, 17, 2),
+    # stride = 2 (mod 4): the merged-word realignment path, every L mod 16 class that
+    # needs the extra carry chunk (15, 0) and short / long rows
+    (158, 2000, 158, 0), (159, 1100, 162, 0), (160, 1300, 162, 0), (14, 700, 14, 0),
+    (46, 1500, 46, 0), (126, 1030, 130, 0), (254, 640, 254, 0), (250, 2100, 250, 0),
+    (2, 300, 2, 0), (175, 999, 178, 0)])
 def test_encode_matches_reference_packer(gk, L, n, stride, offset):
     reads, _ = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED, stride=stride,
                                  emax=max(1, L // 10))
