@@ -282,8 +282,8 @@ static void launch_enc3_t(const uint8_t* seqs, int64_t nblocks, int len, int str
   // registers vs resident CTAs and span buffers per warp, measured per length class
   // (profiles/r02_ab_encoder_minb.jsonl, r02_ab_encoder_nbuf.jsonl): 100 bp double-
   // buffered at 8 CTAs/SM (64 regs; 1.51 -> 1.39 ms per 2 x 30M); 150 bp single-
-  // buffered at 6 (2.40 -> 2.28 ms); 250 bp single-buffered at 5 (3.95 -> 3.51 ms)
-  constexpr int MB = GK_ENC3_MINB > 0 ? GK_ENC3_MINB : (NCH == 7 ? 8 : (NCH == 10 ? 6 : (NCH == 16 ? 5 : 1)));
+  // buffered at 7 (2.40 -> 2.25 ms); 250 bp single-buffered at 5 (3.95 -> 3.51 ms)
+  constexpr int MB = GK_ENC3_MINB > 0 ? GK_ENC3_MINB : (NCH == 7 ? 8 : (NCH == 10 ? 7 : (NCH == 16 ? 5 : 1)));
   constexpr int NB = GK_ENC3_NBUF > 0 ? GK_ENC3_NBUF : (NCH == 7 || NCH == 0 ? 2 : 1);
   const Enc3Cfg c = enc3_cfg(len, stride, NB);
   auto kern = encode3_kernel<NCH, MODE, MB, NB>;
