@@ -124,4 +124,118 @@ __device__ __forceinline__ uint32_t group_undef(const uint32_t (&ag)[4], const u
 }
 
 }  // namespace enc3
+
+// ---- group encoders of encode3_kernel (gk_encode.cu) and the L2-staged fused
+// kernel (gk_fused_l2.cu): outputs collected per block of 4 groups in shared
+// memory, [plane][position * 5 + group]
+template <bool ALN>
+__device__ __forceinline__ void enc3_chunk(const uint8_t* buf, const uint32_t (&roff)[4],
+                                           const uint32_t (&rsh)[4], int c, int len,
+                                           const enc3::Lane& ln, uint32_t (&ag)[4],
+                                           uint32_t (&ay)[4], uint32_t* outs, uint32_t P,
+                                           int wg, bool tail) {
+  uint32_t x[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint8_t* a = buf + roff[i] + 16 * c;
+    uint32_t w;
+    if (ALN) {
+      w = *reinterpret_cast<const uint32_t*>(a);
+    } else {
+      const uint32_t lo = *reinterpret_cast<const uint32_t*>(a);
+      const uint32_t hi = *reinterpret_cast<const uint32_t*>(a + 4);
+      w = __funnelshift_r(lo, hi, rsh[i]);
+    }
+    if (tail) {  // bytes of positions >= len read as 'A' (valid, never stored)
+      const int rem = len - 16 * c - 4 * ln.cw;
+      const uint32_t bm =
+          rem >= 4 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * rem)));
+      w = (w & bm) | (0x41414141u & ~bm);
+    }
+    x[i] = enc3::row_word(w, ln, ag[i], ay[i]);
+  }
+  uint32_t m = enc3::merge4(x[0], x[1], x[2], x[3], ln);
+  m = enc3::transpose3(m, ln);
+  // lane = cw + 4b' + 8k: position 16c + 4cw + k, plane b' (0 = low -> paper plane 1)
+  const int lane = threadIdx.x & 31;
+  const int pos = 16 * c + 4 * (lane & 3) + (lane >> 3);
+  const int plane = ((lane >> 2) & 1) ? 0 : 1;
+  if (!tail || pos < len) outs[plane * P + pos * 5 + wg] = m;
+}
+
+// stride = 2 (mod 4): the rows of a lane all start at the same 2-byte offset
+// (its rows have one parity), so every lane loads ONE aligned word per row (not
+// two + a funnel shift: half the shared-memory loads) and a lane whose rows start
+// 2 bytes into a word realigns its MERGED word instead: in the merged layout
+// (bit = b' + 2i + 8k) a 2-position shift is a 16-bit funnel shift with the
+// merged word of the next column (lane + 1, or for column 3 lane - 3 of the next
+// chunk) -- one SHFL + one SHF per 16 positions.  Chunks are therefore emitted
+// one step late, with one extra load chunk at the end.
+__device__ __forceinline__ uint32_t enc3_merge_m2(const uint8_t* buf, const uint32_t (&roff)[4],
+                                                  int s2, int c, int len, const enc3::Lane& ln,
+                                                  uint32_t (&ag)[4], uint32_t (&ay)[4],
+                                                  bool first, bool tail) {
+  uint32_t x[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t w = *reinterpret_cast<const uint32_t*>(buf + roff[i] + 16 * c);
+    uint32_t bm = 0xFFFFFFFFu;
+    if (first && s2 && ln.cw == 0) bm = 0xFFFF0000u;  // the 2 bytes before the row start
+    if (tail) {
+      const int rem = len - (16 * c + 4 * ln.cw - s2);  // bytes of positions < len
+      bm &= rem >= 4 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * rem)));
+    }
+    if (first || tail) w = (w & bm) | (0x41414141u & ~bm);
+    x[i] = enc3::row_word(w, ln, ag[i], ay[i]);
+  }
+  return enc3::merge4(x[0], x[1], x[2], x[3], ln);
+}
+
+__device__ __forceinline__ void enc3_emit(uint32_t m, int c, int len, const enc3::Lane& ln,
+                                          uint32_t* outs, uint32_t P, int wg) {
+  m = enc3::transpose3(m, ln);
+  const int lane = threadIdx.x & 31;
+  const int pos = 16 * c + 4 * (lane & 3) + (lane >> 3);
+  const int plane = ((lane >> 2) & 1) ? 0 : 1;
+  if (pos < len) outs[plane * P + pos * 5 + wg] = m;
+}
+
+
+// One group's staged span (32 rows at roff / rsh, MODE as encode3_kernel) ->
+// outs[plane * P + pos * 5 + wg] for every position; returns the group's
+// undefined word (bit r = row r).
+template <int NCH, int MODE>
+__device__ __forceinline__ uint32_t enc3_group(const uint8_t* sbuf, const uint32_t (&roff)[4],
+                                               const uint32_t (&rsh)[4], int s2, int len,
+                                               const enc3::Lane& ln, uint32_t* outs, uint32_t P,
+                                               int wg) {
+  const int lane = threadIdx.x & 31;
+  const int nch = NCH > 0 ? NCH : (len + 15) >> 4;
+  uint32_t ag[4] = {0u, 0u, 0u, 0u}, ay[4] = {0u, 0u, 0u, 0u};
+  if constexpr (MODE == 2) {
+    const int cw = ln.cw;
+    const int src = cw == 3 ? lane - 3 : lane + 1;
+    uint32_t prev = enc3_merge_m2(sbuf, roff, s2, 0, len, ln, ag, ay, true, nch <= 1);
+#pragma unroll (NCH > 0 ? NCH : 1)
+    for (int c = 1; c <= nch; ++c) {
+      const uint32_t cur = enc3_merge_m2(sbuf, roff, s2, c, len, ln, ag, ay, false, c >= nch - 1);
+      const uint32_t nxt = __shfl_sync(0xFFFFFFFFu, cw == 0 ? cur : prev, src);
+      enc3_emit(__funnelshift_r(prev, nxt, (uint32_t)(8 * s2)), c - 1, len, ln, outs, P, wg);
+      prev = cur;
+    }
+  } else {
+    constexpr bool ALN = MODE == 0;
+    if (NCH > 0) {
+#pragma unroll
+      for (int c = 0; c < (NCH > 1 ? NCH - 1 : 0); ++c)
+        enc3_chunk<ALN>(sbuf, roff, rsh, c, len, ln, ag, ay, outs, P, wg, false);
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < nch - 1; ++c)
+        enc3_chunk<ALN>(sbuf, roff, rsh, c, len, ln, ag, ay, outs, P, wg, false);
+    }
+    enc3_chunk<ALN>(sbuf, roff, rsh, nch - 1, len, ln, ag, ay, outs, P, wg, true);
+  }
+  return enc3::group_undef(ag, ay, ln);
+}
 }  // namespace gk
