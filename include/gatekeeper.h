@@ -158,25 +158,6 @@ int gk_filter_ascii(const uint8_t* d_reads, const uint8_t* d_refs, int64_t strid
                     int64_t n_pairs, int32_t len, int32_t e,
                     uint32_t* d_accept_bits, uint8_t* d_errcount, void* stream);
 
-/* a1-a6 in one launch from ASCII with the packed tile staged in L2 (the
- * default path of the bench's C5 buckets).  Persistent CTAs loop over tiles of
- * 1024 pairs: encode the tile (as gk_encode) into the CTA's slot of d_ws, then
- * filter it (as gk_filter) from there; the slots are rewritten tile after tile
- * and stay in L2, so the 2-bit planes never round-trip through
- * HBM, and the encoding of one tile overlaps the filtration of another on
- * every SM.  Inputs, outputs and errors as gk_filter_ascii; results identical.
- *  d_ws     : 16-byte aligned device scratch, gk_filter_ascii_workspace_bytes(len)
- *             bytes (fewer bytes = fewer resident CTAs; below one slot of
- *             2*len*256 bytes, or for read lengths / thresholds without an
- *             L2-staged instantiation, the call runs gk_filter_ascii instead).
- *             Owned by the caller; contents undefined afterwards.
- *  ws_bytes : its size in bytes. */
-size_t gk_filter_ascii_workspace_bytes(int32_t len);
-int gk_filter_ascii_ws(const uint8_t* d_reads, const uint8_t* d_refs, int64_t stride,
-                       int64_t n_pairs, int32_t len, int32_t e,
-                       uint32_t* d_accept_bits, uint8_t* d_errcount, void* d_ws,
-                       size_t ws_bytes, void* stream);
-
 /* a1-a6 for EVERY threshold e = 0..e_max in one launch from ASCII: the encode of
  * gk_filter_ascii and the one-pass sweep of gk_filter_sweep fused (one CTA per
  * tile of 1024 pairs; the 2-bit planes stay in shared memory).  Outputs as

@@ -57,8 +57,6 @@ def load_library(path: str = LIB_PATH):
         "gk_filter_sweep": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, I32, P]),
         "gk_filter_ascii": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P]),
         "gk_filter_ascii_sweep": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P]),
-        "gk_filter_ascii_workspace_bytes": (SZ, [I32]),
-        "gk_filter_ascii_ws": (ctypes.c_int, [P, P, I64, I64, I32, I32, P, P, P, SZ, P]),
         "gk_compact_workspace_bytes": (SZ, [I64]),
         "gk_compact": (ctypes.c_int, [P, I64, P, P, P, SZ, P]),
         "gk_compact_rows_workspace_bytes": (SZ, [I64, I32]),
@@ -186,32 +184,6 @@ def filter_ascii(reads, refs, e: int, length: int | None = None, accept=None, er
     _check(load_library().gk_filter_ascii(reads.data_ptr(), refs.data_ptr(), stride, n, length,
                                           e, _ptr(accept), _ptr(errcount), _stream(stream)),
            "gk_filter_ascii")
-    return accept, errcount
-
-
-def filter_ascii_workspace_bytes(length: int) -> int:
-    """Scratch bytes of gk_filter_ascii_ws (one L2-resident tile slot per resident CTA)."""
-    return int(load_library().gk_filter_ascii_workspace_bytes(length))
-
-
-def filter_ascii_ws(reads, refs, e: int, length: int | None = None, accept=None, errcount=None,
-                    workspace=None, want_errcount: bool = True, stream=None):
-    """Fused a1..a6 from ASCII rows with the packed tile staged in L2 (gk_filter_ascii_ws)
-    -> (accept bits, errcount or None).  Same results as filter_ascii."""
-    import torch
-    n, stride = reads.shape
-    length = stride if length is None else length
-    if accept is None:
-        accept = torch.empty(max(1, result_words(n)), dtype=torch.int32, device=reads.device)
-    if errcount is None and want_errcount:
-        errcount = torch.empty(max(1, n), dtype=torch.uint8, device=reads.device)
-    if workspace is None:
-        workspace = torch.empty(filter_ascii_workspace_bytes(length), dtype=torch.uint8,
-                                device=reads.device)
-    _check(load_library().gk_filter_ascii_ws(reads.data_ptr(), refs.data_ptr(), stride, n, length,
-                                             e, _ptr(accept), _ptr(errcount), workspace.data_ptr(),
-                                             workspace.numel(), _stream(stream)),
-           "gk_filter_ascii_ws")
     return accept, errcount
 
 

@@ -155,29 +155,6 @@ int gk_filter_ascii(const uint8_t* d_reads, const uint8_t* d_refs, int64_t strid
   return after_launch();
 }
 
-size_t gk_filter_ascii_workspace_bytes(int32_t len) {
-  if (len <= 0 || len > GK_MAX_LEN) return 0;
-  return gk::fused_l2_workspace_bytes(len);
-}
-
-int gk_filter_ascii_ws(const uint8_t* d_reads, const uint8_t* d_refs, int64_t stride,
-                       int64_t n_pairs, int32_t len, int32_t e, uint32_t* d_accept_bits,
-                       uint8_t* d_errcount, void* d_ws, size_t ws_bytes, void* stream) {
-  int rc = check_ascii(d_reads, n_pairs, len, stride);
-  if (rc) return rc;
-  if (n_pairs > 0 && d_refs == nullptr) return GK_ERR_ARG;
-  if (e < 0 || e >= len) return GK_ERR_E;
-  if (n_pairs == 0) return GK_OK;
-  if (!d_accept_bits) return GK_ERR_ARG;
-  if (!aligned(d_accept_bits, 4)) return GK_ERR_ALIGN;
-  if (d_ws != nullptr && !aligned(d_ws, 16)) return GK_ERR_ALIGN;
-  if (!gk::launch_fused_l2(d_reads, d_refs, stride, n_pairs, len, e, d_ws, ws_bytes,
-                           d_accept_bits, d_errcount, (cudaStream_t)stream))
-    gk::launch_filter_ascii(d_reads, d_refs, stride, n_pairs, len, e, d_accept_bits, d_errcount,
-                            (cudaStream_t)stream);
-  return after_launch();
-}
-
 int gk_filter_ascii_sweep(const uint8_t* d_reads, const uint8_t* d_refs, int64_t stride,
                           int64_t n_pairs, int32_t len, int32_t e_max, uint32_t* d_accept_bits,
                           uint8_t* d_errcount, void* stream) {

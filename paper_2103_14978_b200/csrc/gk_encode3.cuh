@@ -125,9 +125,8 @@ __device__ __forceinline__ uint32_t group_undef(const uint32_t (&ag)[4], const u
 
 }  // namespace enc3
 
-// ---- group encoders of encode3_kernel (gk_encode.cu) and the L2-staged fused
-// kernel (gk_fused_l2.cu): outputs collected per block of 4 groups in shared
-// memory, [plane][position * 5 + group]
+// ---- group encoder of encode3_kernel (gk_encode.cu): outputs collected per
+// block of 4 groups in shared memory, [plane][position * 5 + group]
 template <bool ALN>
 __device__ __forceinline__ void enc3_chunk(const uint8_t* buf, const uint32_t (&roff)[4],
                                            const uint32_t (&rsh)[4], int c, int len,

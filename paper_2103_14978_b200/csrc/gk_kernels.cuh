@@ -31,12 +31,6 @@ int launch_filter_ascii(const uint8_t* reads, const uint8_t* refs, int64_t strid
 bool launch_fused(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n, int len,
                   int e, bool sweep, uint32_t* accept, uint8_t* errc, cudaStream_t stream);
 
-// L2-staged fused ASCII kernel (gk_fused_l2.cu); false = cannot take the call
-size_t fused_l2_workspace_bytes(int len);
-bool launch_fused_l2(const uint8_t* reads, const uint8_t* refs, int64_t stride, int64_t n,
-                     int len, int e, void* ws, size_t ws_bytes, uint32_t* accept, uint8_t* errc,
-                     cudaStream_t stream);
-
 size_t compact_workspace_bytes(int64_t n, int rows = 1);
 // ibase is added to every written index (chunked host pipelines: absolute indices)
 int launch_compact(const uint32_t* bits, int64_t n, uint32_t* idx, uint64_t* n_acc, void* ws,
