@@ -71,6 +71,23 @@ __device__ __forceinline__ void mask_and_checked(const Win<B>& R, const Win<B>& 
   for (int u = 0; u < B; ++u) F[u] &= amend(x[u], x[u + 1], x[u + 2], x[u + 3], x[u + 4]) | vac[u];
 }
 
+// Add N words of weight 2^P into bit-sliced planes pl[P..NP): a carry-save tree
+// (full adders in pairs, a half adder for an odd word out), carries to P+1.
+template <int P, int NP, int N>
+__device__ __forceinline__ void csa_add(uint32_t (&pl)[NP], const uint32_t (&w)[N]) {
+  if constexpr (N > 0 && P < NP) {
+    constexpr int NN = N / 2 + (N & 1);
+    uint32_t c[NN];
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) CsaCounter::fa(pl[P], w[2 * i], w[2 * i + 1], c[i]);
+    if constexpr (N & 1) {
+      c[NN - 1] = pl[P] & w[N - 1];
+      pl[P] ^= w[N - 1];
+    }
+    csa_add<P + 1, NP, NN>(pl, c);
+  }
+}
+
 // Per-k run-start counter of the sweep in shared memory: NP bit-sliced planes of
 // 32 lanes (bank = lane).  Windows start at multiples of 4 and ib % B == 0, so a
 // block's starts never depend on the previous block (readings R6, R7).
@@ -82,34 +99,7 @@ __device__ __forceinline__ void count_block_smem(uint32_t* p, const uint32_t (&F
   uint32_t pl[NP];
 #pragma unroll
   for (int b = 0; b < NP; ++b) pl[b] = p[b * 32];
-  // carry-save tree: B words into planes 0..; the carries ripple upwards
-  uint32_t c1[B / 2];
-#pragma unroll
-  for (int i = 0; i < B / 2; ++i) CsaCounter::fa(pl[0], st[2 * i], st[2 * i + 1], c1[i]);
-  uint32_t c2[B / 4];
-#pragma unroll
-  for (int i = 0; i < B / 4; ++i) CsaCounter::fa(pl[1], c1[2 * i], c1[2 * i + 1], c2[i]);
-  uint32_t f;
-  if constexpr (B == 8) {
-    CsaCounter::fa(pl[2], c2[0], c2[1], f);
-#pragma unroll
-    for (int b = 3; b < NP; ++b) {
-      const uint32_t t = pl[b] & f;
-      pl[b] ^= f;
-      f = t;
-    }
-  } else {  // B == 16
-    uint32_t c3[2];
-    CsaCounter::fa(pl[2], c2[0], c2[1], c3[0]);
-    CsaCounter::fa(pl[2], c2[2], c2[3], c3[1]);
-    CsaCounter::fa(pl[3], c3[0], c3[1], f);
-#pragma unroll
-    for (int b = 4; b < NP; ++b) {
-      const uint32_t t = pl[b] & f;
-      pl[b] ^= f;
-      f = t;
-    }
-  }
+  csa_add<0, NP, B>(pl, st);
 #pragma unroll
   for (int b = 0; b < NP; ++b) p[b * 32] = pl[b];
 }
@@ -120,11 +110,17 @@ __device__ __forceinline__ void count_block_reg(const uint32_t (&M)[B], CsaCount
 #pragma unroll
   for (int u = 0; u < B; ++u) s[u] = (u & 3) ? (M[u] & ~M[u - 1]) : M[u];
 #pragma unroll
-  for (int h = 0; h < B; h += 8) {
+  for (int h = 0; h + 8 <= B; h += 8) {
     uint32_t s8[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) s8[u] = s[h + u];
     c.add8(s8);
+  }
+  if constexpr (B % 8 == 4) {
+    uint32_t s4[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s4[u] = s[B - 4 + u];
+    c.add4(s4);
   }
 }
 

@@ -37,14 +37,20 @@ namespace gk {
 #define GK_BT2_B_E 16   // positions per block of the per-e kernel (2 CTAs/SM, 252 regs)
 #endif
 #ifndef GK_BT2_MINB
-#define GK_BT2_MINB 2
+#define GK_BT2_MINB 2   // resident CTAs per SM asked of ptxas (per-e kernel)
+#endif
+#ifndef GK_BT2_E_WARPS
+#define GK_BT2_E_WARPS 4  // warps (tiles) per CTA of the per-e kernel
 #endif
 #ifndef GK_BT2_SWEEP_MINB
 #define GK_BT2_SWEEP_MINB 6
 #endif
+#ifndef GK_BT2_SWEEP_B16_LEN
+#define GK_BT2_SWEEP_B16_LEN 200  // reads at least this long take 16-position sweep blocks
+#endif
 
 template <int B>
-__global__ void __launch_bounds__(128, GK_BT2_MINB) filter_bt2_kernel(
+__global__ void __launch_bounds__(GK_BT2_E_WARPS * 32, GK_BT2_MINB) filter_bt2_kernel(
     const uint2* __restrict__ reads, const uint2* __restrict__ refs,
     const uint32_t* __restrict__ rund, const uint32_t* __restrict__ fund, int64_t n, int len, int e,
     uint32_t* __restrict__ accept, uint8_t* __restrict__ errc, int edge_fix) {
@@ -68,10 +74,13 @@ __global__ void __launch_bounds__(128, GK_BT2_MINB) filter_bt2_kernel(
   if (g * 32 < n) finish_group(a, f, e, __ldg(rund + g) | __ldg(fund + g), g, n, accept, errc);
 }
 
-constexpr int BT2_SWEEP_WARPS = 2;
+#ifndef GK_BT2_SWEEP_WARPS
+#define GK_BT2_SWEEP_WARPS 2
+#endif
+constexpr int BT2_SWEEP_WARPS = GK_BT2_SWEEP_WARPS;
 
-template <int B, int NP>
-__global__ void __launch_bounds__(BT2_SWEEP_WARPS * 32, GK_BT2_SWEEP_MINB) filter_bt2_sweep_kernel(
+template <int B, int NP, int MINB>
+__global__ void __launch_bounds__(BT2_SWEEP_WARPS * 32, MINB) filter_bt2_sweep_kernel(
     const uint2* __restrict__ reads, const uint2* __restrict__ refs,
     const uint32_t* __restrict__ rund, const uint32_t* __restrict__ fund, int64_t n, int len,
     int emax, uint32_t* __restrict__ accept, uint8_t* __restrict__ errc, int edge_fix) {
@@ -118,7 +127,7 @@ void launch_bt2(const uint2* reads, const uint2* refs, const uint32_t* rund, con
                 cudaStream_t stream) {
   constexpr int B = GK_BT2_B_E;
   const int64_t tiles = (n + 1023) / 1024;
-  const int warps = 4;
+  const int warps = GK_BT2_E_WARPS;
   const int64_t blocks = (tiles + warps - 1) / warps;
   static thread_local bool attr_set = false;  // L1 carveout: once per thread
   if (!attr_set) {
@@ -130,37 +139,51 @@ void launch_bt2(const uint2* reads, const uint2* refs, const uint32_t* rund, con
                                                                     len, e, accept, errc, edge_fix);
 }
 
-template <int NP>
+template <int B, int NP, int MINB>
 static void launch_bt2_sweep_np(const uint2* reads, const uint2* refs, const uint32_t* rund,
                                 const uint32_t* fund, int64_t n, int len, int emax,
                                 uint32_t* accept, uint8_t* errc, int edge_fix,
                                 cudaStream_t stream) {
-  constexpr int B = GK_BT2_B;
   const int64_t tiles = (n + 1023) / 1024;
   const int64_t blocks = (tiles + BT2_SWEEP_WARPS - 1) / BT2_SWEEP_WARPS;
   const size_t smem = (size_t)BT2_SWEEP_WARPS * emax * NP * 32 * 4;
   static thread_local size_t attr_smem = 0;
   if (smem > 48 * 1024 && smem > attr_smem) {
-    cudaFuncSetAttribute(filter_bt2_sweep_kernel<B, NP>,
+    cudaFuncSetAttribute(filter_bt2_sweep_kernel<B, NP, MINB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_smem = smem;
   }
   count_launch();
-  filter_bt2_sweep_kernel<B, NP><<<(unsigned)blocks, BT2_SWEEP_WARPS * 32, smem, stream>>>(
+  filter_bt2_sweep_kernel<B, NP, MINB><<<(unsigned)blocks, BT2_SWEEP_WARPS * 32, smem, stream>>>(
       reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix);
 }
 
 void launch_bt2_sweep(const uint2* reads, const uint2* refs, const uint32_t* rund,
                       const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,
                       uint8_t* errc, int edge_fix, cudaStream_t stream) {
-  // counter planes: enough bits for the largest count, 2 * ceil(len / 4) (R6, R7)
+  // counter planes: enough bits for the largest count, 2 * ceil(len / 4) (R6, R7).
+  // Block size by read length (profiles/r02_ab_sweep_block.jsonl, 30M pairs): 8-position
+  // blocks at 6 CTAs/SM (157 regs, 12 warps) are fastest at 100 / 150 bp; 16-position
+  // blocks (1.1x instead of 1.2x the model's mismatch work; 255 regs, 8 warps) at
+  // 250 bp (7.17 -> 6.65 ms at e_max = 25).
   const int maxc = 2 * ((len + 3) / 4);
-  if (maxc < 64)
-    launch_bt2_sweep_np<6>(reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix, stream);
-  else if (maxc < 128)
-    launch_bt2_sweep_np<7>(reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix, stream);
-  else
-    launch_bt2_sweep_np<8>(reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix, stream);
+  if (len >= GK_BT2_SWEEP_B16_LEN) {
+    if (maxc < 128)
+      launch_bt2_sweep_np<16, 7, 4>(reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix,
+                                    stream);
+    else
+      launch_bt2_sweep_np<16, 8, 4>(reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix,
+                                    stream);
+  } else if (maxc < 64) {
+    launch_bt2_sweep_np<GK_BT2_B, 6, GK_BT2_SWEEP_MINB>(reads, refs, rund, fund, n, len, emax,
+                                                        accept, errc, edge_fix, stream);
+  } else if (maxc < 128) {
+    launch_bt2_sweep_np<GK_BT2_B, 7, GK_BT2_SWEEP_MINB>(reads, refs, rund, fund, n, len, emax,
+                                                        accept, errc, edge_fix, stream);
+  } else {
+    launch_bt2_sweep_np<GK_BT2_B, 8, GK_BT2_SWEEP_MINB>(reads, refs, rund, fund, n, len, emax,
+                                                        accept, errc, edge_fix, stream);
+  }
 }
 
 }  // namespace gk

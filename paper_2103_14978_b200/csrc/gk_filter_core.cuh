@@ -73,6 +73,16 @@ struct CsaCounter {
     fa(fours, d0, d1, f0);
     add_up(f0);
   }
+  // four start words (3 full adders + one ripple)
+  __host__ __device__ __forceinline__ void add4(const uint32_t (&s)[4]) {
+    uint32_t c0, c1, d0;
+    fa(ones, s[0], s[1], c0);
+    fa(ones, s[2], s[3], c1);
+    fa(twos, c0, c1, d0);
+    const uint32_t f = fours & d0;
+    fours ^= d0;
+    add_up(f);
+  }
   __host__ __device__ __forceinline__ void planes(uint32_t (&c)[8]) const {
     c[0] = ones;
     c[1] = twos;
