@@ -119,7 +119,6 @@ __global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restr
   }
   const int s2 = (int)(rsh[0] >> 3);  // MODE 2: the lane's rows start 0 or 2 bytes into a word
   const uint32_t span = 32u * (uint32_t)stride;
-  const int nch = NCH > 0 ? NCH : (len + 15) >> 4;
 
   int64_t b = blockIdx.x;
   if (b >= nblocks) return;
