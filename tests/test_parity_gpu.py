@@ -222,8 +222,11 @@ def test_sweep_kernel_paper_profile(gk, L):
     assert_sweep_parity(gk, reads, refs, {100: 10, 150: 15, 250: 25}[L])
 
 
-@pytest.mark.parametrize("L", [1, 2, 3, 5, 8, 9, 16, 17, 31, 33, 64, 100, 129, 255, 508])
+@pytest.mark.parametrize("L", [1, 2, 3, 5, 8, 9, 16, 17, 31, 33, 64, 100, 129, 199, 200, 201,
+                               212, 255, 508])
 def test_sweep_kernel_random_lengths(gk, L):
+    """Every length class of the sweep dispatch (8-position blocks below 200 bp,
+    16-position blocks from 200 bp; ragged last blocks)."""
     n = 1500 if L < 300 else 600
     reads, refs = pairgen.gen_pairs(n, L, profile=pairgen.PROFILE_BALANCED,
                                     emax=max(1, L // 10), seed=L + 7)
@@ -252,11 +255,11 @@ def test_sweep_many_thresholds_fallback(gk):
     reads, refs = pairgen.gen_pairs(600, L, profile=pairgen.PROFILE_BALANCED, emax=40, seed=3)
     a, c = run_sweep(gk, reads, refs, emax)
     oa, oc = oracle.sweep(reads, refs, emax)
-    for e in range(0, emax + 1, 23):
+    for e in range(emax + 1):
         assert (a[e] == oa[e]).all() and (c[e] == oc[e]).all(), e
 
 
-@pytest.mark.parametrize("L", [17, 100])
+@pytest.mark.parametrize("L", [17, 100, 250])
 def test_sweep_kernel_original_gatekeeper(gk, L):
     reads, refs = pairgen.gen_pairs(2000, L, profile=pairgen.PROFILE_BALANCED, emax=L // 10 + 1,
                                     seed=L + 1234)
