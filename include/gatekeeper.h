@@ -211,9 +211,12 @@ int gk_compact_rows(const uint32_t* d_accept_bits, int32_t n_rows, int64_t bits_
 size_t gk_plane_words(int64_t n_bases);
 
 /* ASCII rows -> bit planes: base i of row r (byte d_rows[r*stride + i], i < len)
- * is base r*len + i of the planes (n_bases = n_rows*len; a genome is one row).
+ * is base r*len + i of the planes (n_bases = n_rows*len; a genome is one row:
+ * len is 64-bit, so a whole GRCh37-sized genome, ~3.1 Gbases, fits one row).
+ * Contiguous input (one row, or stride == len) at a 16-byte aligned d_rows takes
+ * the coalesced 16-byte-load path; any other layout is read byte by byte.
  * Errors: GK_ERR_ARG, GK_ERR_LEN, GK_ERR_ALIGN, GK_ERR_CUDA. */
-int gk_pack_planes(const uint8_t* d_rows, int64_t n_rows, int32_t len, int64_t stride,
+int gk_pack_planes(const uint8_t* d_rows, int64_t n_rows, int64_t len, int64_t stride,
                    uint32_t* d_planes, void* stream);
 
 /* Windows -> the packed layout gk_filter / gk_filter_sweep consume: sequence p

@@ -65,7 +65,7 @@ def load_library(path: str = LIB_PATH):
         "gk_host_index_workspace_bytes": (SZ, [I64, I32, I32]),
         "gk_filter_host_index": (ctypes.c_int, [P, I64, P, I64, P, P, I64, I32, I32, P, P, P, SZ,
                                                 I64, P]),
-        "gk_pack_planes": (ctypes.c_int, [P, I64, I32, I64, P, P]),
+        "gk_pack_planes": (ctypes.c_int, [P, I64, I64, I64, P, P]),
         "gk_gather_windows": (ctypes.c_int, [P, I64, P, I64, I32, P, P, P]),
         "gk_accuracy": (ctypes.c_int, [P, I64, P, I64, P, I64, P, I32, P, P]),
         "gk_compact_rows": (ctypes.c_int, [P, I32, I64, I64, P, I64, P, P, SZ, P]),
@@ -207,14 +207,23 @@ def filter_ascii_sweep(reads, refs, e_max: int, length: int | None = None, accep
 
 
 # ---- a7: compact --------------------------------------------------------------
+def _check_index_range(n: int):
+    if n >= 1 << 31:
+        raise GateKeeperError(f"compact: n = {n} >= 2^31 would return negative int32 indices; "
+                              "split the batch (the C ABI itself takes n < 2^32)")
+
+
 def compact_workspace_bytes(n: int) -> int:
     return load_library().gk_compact_workspace_bytes(n)
 
 
 def compact(accept, n: int, idx=None, n_acc=None, workspace=None, want_indices: bool = True,
             stream=None):
-    """Ordered indices of accepted pairs -> (idx u32[n] (first n_acc valid), n_acc u64[1])."""
+    """Ordered indices of accepted pairs -> (idx u32[n] (first n_acc valid), n_acc u64[1]).
+    The indices are u32 (the C ABI's); the default idx tensor is int32, so n is capped
+    below 2^31 here (pass a larger int32 buffer viewed as u32 to the C ABI directly)."""
     import torch
+    _check_index_range(n)
     dev = accept.device
     if idx is None and want_indices:
         idx = torch.empty(max(1, n), dtype=torch.int32, device=dev)
@@ -236,8 +245,10 @@ def compact_rows_workspace_bytes(n: int, rows: int) -> int:
 def compact_rows(accept, n: int, idx=None, n_acc=None, workspace=None, want_indices: bool = True,
                  stream=None):
     """a7 for every row of a 2-D accept tensor [rows, >= ceil(n/32)] (e.g. filter_sweep's)
-    in one launch pair -> (idx u32 [rows, n] or None, n_acc i64 [rows])."""
+    in one launch pair -> (idx u32 [rows, n] or None, n_acc i64 [rows]); n < 2^31 (see
+    compact)."""
     import torch
+    _check_index_range(n)
     rows = accept.shape[0]
     dev = accept.device
     if idx is None and want_indices:

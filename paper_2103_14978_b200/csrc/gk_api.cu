@@ -14,7 +14,7 @@ int launch_edit_distance(const uint8_t* reads, const uint8_t* refs, int64_t stri
 int launch_accuracy(const uint32_t* accept, int64_t astride, const uint8_t* errc, int64_t estride,
                     const int32_t* dist, int64_t n, const int32_t* e_list, int rows,
                     unsigned long long* counts, cudaStream_t stream);
-int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int len, int64_t stride,
+int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int64_t len, int64_t stride,
                        uint32_t* planes, cudaStream_t stream);
 int launch_gather_windows(const uint32_t* planes, int64_t nbases, const int64_t* offsets, int64_t n,
                           int len, uint32_t* packed, uint32_t* undef, cudaStream_t stream);
@@ -218,7 +218,7 @@ size_t gk_plane_words(int64_t n_bases) {
   return (size_t)((n_bases + 31) / 32 + 1);
 }
 
-int gk_pack_planes(const uint8_t* d_rows, int64_t n_rows, int32_t len, int64_t stride,
+int gk_pack_planes(const uint8_t* d_rows, int64_t n_rows, int64_t len, int64_t stride,
                    uint32_t* d_planes, void* stream) {
   if (n_rows < 0 || stride < len) return GK_ERR_ARG;
   if (len < 1) return GK_ERR_LEN;

@@ -19,26 +19,78 @@
 namespace gk {
 
 // ---- packing: ASCII rows -> bit planes ----------------------------------------
-// One thread per 32 consecutive bases of the concatenation (row r, base i) ->
-// bit r*len + i.  Code: high = ASCII bit 2, low = bit 1 ^ bit 2 (as gk_encode);
-// undefined = not one of A C G T a c g t.
-__global__ void pack_planes_kernel(const uint8_t* __restrict__ rows, int64_t n_rows, int len,
+// Code: high = ASCII bit 2, low = bit 1 ^ bit 2 (as gk_encode); undefined = not
+// one of A C G T a c g t (its code bits are 0).  Base r*len + i of the
+// concatenation is bit (r*len+i) % 32 of plane word (r*len+i) / 32.
+//
+// Contiguous rows (one row -- a genome -- or stride == len): lane = plane word,
+// its 32 bases are 32 contiguous bytes (two 16-byte loads; a warp reads 1 KB
+// contiguous), decoded 4 bytes at a time with SWAR tests and a multiply-gather
+// of the 4 byte bits into a nibble.  Other strides: one byte load per base.
+
+// bits 0, 8, 16, 24 of y -> bits 0..3 (the partial products y_k * 2^(7m) land on
+// distinct bits 8k+7m, so there are no carries; k+m = 3 gives bits 21..24)
+__device__ __forceinline__ uint32_t gather4(uint32_t y) { return (y * 0x00204081u) >> 21 & 0xFu; }
+
+// 4 ASCII bytes -> hi / lo / undefined nibbles (bit k = byte k)
+__device__ __forceinline__ void decode4(uint32_t w, uint32_t& hn, uint32_t& ln, uint32_t& un) {
+  const uint32_t x = (w ^ (w >> 1)) & 0x06060606u;  // lo at bit 1, hi at bit 2 of each byte
+  // validity as gk_encode (gk_encode3.cuh row_word): bits 7,6,3 = 0,1,0 and
+  // b4 == b2 & ~b1, b0 != b4
+  const uint32_t y = w ^ 0x40404040u;
+  const uint32_t g = (w ^ ((w << 2) & ~(w << 3))) | ~(w ^ (w << 4));
+  const uint32_t bad = ((g >> 4) | (y >> 3) | (y >> 6) | (y >> 7)) & 0x01010101u;
+  un = gather4(bad);
+  hn = gather4((x >> 2) & 0x01010101u) & ~un;
+  ln = gather4((x >> 1) & 0x01010101u) & ~un;
+}
+
+__global__ void pack_planes_contig_kernel(const uint8_t* __restrict__ seq, int64_t total,
+                                          uint4* __restrict__ planes, int64_t nwords) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = 0u, l = 0u, u = 0u;
+    const int64_t b0 = w * 32;
+    if (b0 + 32 <= total) {
+      const uint4* src = reinterpret_cast<const uint4*>(seq + b0);
+      const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
+      const uint32_t q[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t hn, ln, un;
+        decode4(q[k], hn, ln, un);
+        h |= hn << (4 * k);
+        l |= ln << (4 * k);
+        u |= un << (4 * k);
+      }
+    } else {  // the last (partial) word and the look-ahead word: bytes < total only
+      for (int k = 0; k < 32 && b0 + k < total; ++k) {
+        uint32_t hn, ln, un;
+        decode4(__ldg(seq + b0 + k), hn, ln, un);
+        h |= (hn & 1u) << k;
+        l |= (ln & 1u) << k;
+        u |= (un & 1u) << k;
+      }
+    }
+    planes[w] = make_uint4(h, l, u, 0u);
+  }
+}
+
+__global__ void pack_planes_kernel(const uint8_t* __restrict__ rows, int64_t n_rows, int64_t len,
                                    int64_t stride, uint4* __restrict__ planes, int64_t nwords) {
-  const int64_t total = n_rows * (int64_t)len;
+  const int64_t total = n_rows * len;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
        w += (int64_t)gridDim.x * blockDim.x) {
     uint32_t h = 0u, l = 0u, b = 0u;
     int64_t idx = w * 32;
     int64_t r = idx / len;
-    int i = (int)(idx - r * len);
+    int64_t i = idx - r * len;
     for (int k = 0; k < 32 && idx + k < total; ++k) {
-      const uint32_t c = __ldg(rows + r * stride + i);
-      const uint32_t u = c & 0xDFu;  // upper case
-      const bool valid = u == 'A' || u == 'C' || u == 'G' || u == 'T';
-      const uint32_t b2 = (c >> 2) & 1u, b1 = (c >> 1) & 1u;
-      h |= (valid ? b2 : 0u) << k;
-      l |= (valid ? (b1 ^ b2) : 0u) << k;
-      b |= (valid ? 0u : 1u) << k;
+      uint32_t hn, ln, un;
+      decode4(__ldg(rows + r * stride + i), hn, ln, un);
+      h |= (hn & 1u) << k;
+      l |= (ln & 1u) << k;
+      b |= (un & 1u) << k;
       if (++i == len) {
         i = 0;
         ++r;
@@ -48,15 +100,20 @@ __global__ void pack_planes_kernel(const uint8_t* __restrict__ rows, int64_t n_r
   }
 }
 
-int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int len, int64_t stride,
+int launch_pack_planes(const uint8_t* rows, int64_t n_rows, int64_t len, int64_t stride,
                        uint32_t* planes, cudaStream_t stream) {
-  const int64_t total = n_rows * (int64_t)len;
+  const int64_t total = n_rows * len;
   const int64_t nwords = (total + 31) / 32 + 1;  // + 1: the funnel shift's look-ahead word
   int64_t blocks = (nwords + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   count_launch();
-  pack_planes_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rows, n_rows, len, stride,
-                                                           reinterpret_cast<uint4*>(planes), nwords);
+  if ((n_rows == 1 || stride == len) && (reinterpret_cast<uintptr_t>(rows) & 15u) == 0)
+    pack_planes_contig_kernel<<<(unsigned)blocks, 256, 0, stream>>>(
+        rows, total, reinterpret_cast<uint4*>(planes), nwords);
+  else
+    pack_planes_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rows, n_rows, len, stride,
+                                                             reinterpret_cast<uint4*>(planes),
+                                                             nwords);
   return 0;
 }
 

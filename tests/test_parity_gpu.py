@@ -320,6 +320,50 @@ def make_index_case(G, n_reads, n_cand, L, seed):
     return genome, reads, read_id.astype(np.int64), pos.astype(np.int64)
 
 
+def _planes_expected(seq: np.ndarray) -> np.ndarray:
+    """(hi, lo, undef, 0) words of a base sequence, from the oracle's per-byte code
+    (-1 = undefined) -- bit b of word w is base 32w + b."""
+    codes = np.array([oracle.code(int(b)) for b in range(256)])[seq]
+    n = seq.size
+    words = (n + 31) // 32 + 1
+    bits = np.zeros((3, words * 32), np.uint8)
+    bits[0, :n] = (codes >= 0) & ((codes >> 1) & 1 == 1)
+    bits[1, :n] = (codes >= 0) & (codes & 1 == 1)
+    bits[2, :n] = codes < 0
+    out = np.zeros((words, 4), np.uint32)
+    for p in range(3):
+        out[:, p] = np.packbits(bits[p].reshape(words, 32), axis=1, bitorder="little").view(np.uint32)[:, 0]
+    return out
+
+
+@pytest.mark.parametrize("case", ["genome", "rows", "rows_strided", "unaligned", "random_bytes"])
+def test_pack_planes(gk, case):
+    """gk_pack_planes (coalesced path for contiguous input, byte path otherwise) ==
+    the oracle's per-base code, bit for bit, incl. the ragged last word and the zero
+    look-ahead word."""
+    rng = np.random.default_rng(11)
+    alpha = np.frombuffer(b"ACGTacgtNRY-", np.uint8)
+    if case == "random_bytes":
+        rows = rng.integers(0, 256, (1, 70_001), dtype=np.uint8)
+    else:
+        rows = alpha[rng.choice(len(alpha), (1, 100_003), p=[.22] * 4 + [.02] * 4 + [.01] * 4)]
+    if case in ("rows", "rows_strided", "unaligned"):
+        rows = rows[:, :99_000].reshape(990, 100)
+    L = rows.shape[1]
+    if case == "rows_strided":
+        dev = to_dev(np.concatenate([rows, np.zeros((rows.shape[0], 7), np.uint8)], 1))
+    elif case == "unaligned":
+        flat = to_dev(np.concatenate([np.zeros(3, np.uint8), rows.reshape(-1)]))
+        dev = flat[3:].view(rows.shape[0], L)
+    else:
+        dev = to_dev(rows)
+    planes = gk.pack_planes(dev, length=L)
+    torch.cuda.synchronize()
+    got = planes.cpu().numpy().view(np.uint32)
+    exp = _planes_expected(rows.reshape(-1))
+    assert got.shape == exp.shape and (got == exp).all(), np.argwhere(got != exp)[:5]
+
+
 @pytest.mark.parametrize("L,emax", [(100, 10), (150, 15), (37, 6), (250, 25)])
 def test_reference_index_mode(gk, L, emax):
     """pack_planes + gather_windows + filter_sweep == the oracle on the ASCII
