@@ -180,7 +180,11 @@ int launch_filter_sweep(const uint32_t* reads, const uint32_t* refs, const uint3
                         uint8_t* errc, int flags, cudaStream_t stream) {
   // the one-pass kernel keeps emax counters of up to 8 planes per warp in shared
   // memory (2 warps per CTA): beyond ~100 thresholds they no longer fit, and the
-  // rows are produced by one gk_filter launch per e instead (same results)
+  // rows are produced by one gk_filter launch per e instead (same results).  The
+  // cut-off is by capacity, not occupancy, on purpose: near it only 1-2 CTAs (2-4
+  // warps) fit an SM, but the per-e fallback evaluates sum_e (2e+1) = (e_max+1)^2
+  // mask passes instead of 2 e_max + 1 (26x more at e_max = 50), which no
+  // occupancy gain can make up
   const int maxc = 2 * ((len + 3) / 4);
   const int np = maxc < 64 ? 6 : (maxc < 128 ? 7 : 8);
   const size_t smem = (size_t)2 * emax * np * 32 * 4;
