@@ -26,6 +26,9 @@
 #ifndef GK_ENC3_MINB
 #define GK_ENC3_MINB 0  // 0: per length class (launch_enc3_t)
 #endif
+#ifndef GK_ENC3_PF
+#define GK_ENC3_PF 0  // L2 prefetch distance in blocks (A/B knob; 1-2 measured 1.1-1.5x slower)
+#endif
 #ifndef GK_ENCODE_TMA
 #define GK_ENCODE_TMA 1
 #endif
@@ -129,6 +132,14 @@ __global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restr
   for (int it = 0; b < nblocks; ++it, b += gridDim.x) {
     const int buf = NB == 2 ? (it & 1) : 0;
     const int64_t bn = b + gridDim.x;
+    if (GK_ENC3_PF > 0 && lane == 0) {  // L2 prefetch of the span GK_ENC3_PF blocks past bn
+      const int64_t bp = bn + (int64_t)GK_ENC3_PF * gridDim.x;
+      if (bp < nblocks)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                         seqs + (4 * bp + warp) * (int64_t)span),
+                     "r"(span)
+                     : "memory");
+    }
     if (NB == 2 && lane == 0 && bn < nblocks) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&mybar[buf ^ 1], span);

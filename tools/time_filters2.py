@@ -48,6 +48,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--per-e", nargs="*", default=["250:12"])
     ap.add_argument("--sweep", nargs="*", default=[])
+    ap.add_argument("--encode", nargs="*", type=int, default=[], help="read lengths: time gk_encode x2")
     ap.add_argument("--n", type=int, default=30_000_000)
     ap.add_argument("--tag", default=os.path.basename(os.environ.get("GK_LIB", "default")))
     a = ap.parse_args()
@@ -66,6 +67,17 @@ def main():
             cache[L] = (q, s, uq, us)
         return cache[L]
 
+    for L in a.encode:
+        cache.clear()
+        torch.cuda.empty_cache()
+        r, f = pairgen.gen_pairs_cuda(a.n, L)
+        q, uq = gk.encode(r, L)
+        s, us = gk.encode(f, L)
+        res[f"{L}bp_encode_x2_ms"] = round(timed(lambda: (gk.encode(r, L, out=(q, uq)),
+                                                          gk.encode(f, L, out=(s, us)))), 4)
+        res[f"{L}bp_encode_GB_s"] = round(a.n * 2 * (L + L / 4) / (res[f"{L}bp_encode_x2_ms"] / 1e3) / 1e9, 1)
+        res[f"{L}bp_encode_sum"] = checksum(q, s, uq, us)
+        del r, f, q, s, uq, us
     for spec in a.per_e:
         L, e = map(int, spec.split(":"))
         q, s, uq, us = packed(L)
