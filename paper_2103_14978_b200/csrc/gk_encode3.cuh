@@ -59,9 +59,11 @@ struct Lane {
   uint32_t rot[3];                    // rotate amounts
   int rows[4];                        // r_i
   int cw;
+  uint32_t lofix;                     // ~0 on the lanes that hold a low-plane word (b' = 0)
   __device__ __forceinline__ void init(int lane) {
     m2 = 2u; m4 = 4u; m8 = 8u; m16 = 16u; m32 = 32u; mh = 0x80000000u;
     cw = lane & 3;
+    lofix = ((lane >> 2) & 1) ? 0u : 0xFFFFFFFFu;
     const int rh0 = (lane >> 2) & 1, rh1 = (lane >> 3) & 1, rh2 = (lane >> 4) & 1;
 #pragma unroll
     for (int i = 0; i < 4; ++i) rows[i] = rh0 + 2 * i + 8 * rh1 + 16 * rh2;
@@ -123,7 +125,47 @@ __device__ __forceinline__ uint32_t group_undef(const uint32_t (&ag)[4], const u
   return __reduce_or_sync(0xFFFFFFFFu, u);
 }
 
+// GK_ENC3_RAW = 1: merge the RAW ASCII bits 1 and 2 of the 4 rows (bit-field
+// selects, no per-row code arithmetic) and form the low plane b1 ^ b2 AFTER the
+// transpose: the transpose is a bit permutation, so XOR commutes with it, and
+// lane l (b' = 0, raw b1) XORs the word of lane l ^ 4 (b' = 1, raw b2 = the high
+// plane).  Per 16 positions: 4 fewer ALU shifts + 4 fewer LOP3 for 1 SHFL + 1 LOP3.
+// Validity as row_word; `s3` = w << 3 is passed in (row 2 shares it with the merge).
+__device__ __forceinline__ void row_valid(uint32_t w, uint32_t s3, const Lane& ln, uint32_t& acc_g,
+                                          uint32_t& acc_y) {
+  const uint32_t s2 = imul(w, ln.m4), s4 = imul(w, ln.m16);
+  const uint32_t h = w ^ (s2 & ~s3);
+  acc_g |= h | ~(w ^ s4);
+  acc_y |= w ^ 0x40404040u;
+}
+
+// bit b' + 2i + 8k = ASCII bit (1 + b') of row i, byte k; also the validity of the rows
+__device__ __forceinline__ uint32_t merge4_raw(const uint32_t (&w)[4], const Lane& ln,
+                                               uint32_t (&ag)[4], uint32_t (&ay)[4]) {
+  const uint32_t a = w[0] >> 1;
+  const uint32_t b = imul(w[1], ln.m2);   // << 1
+  const uint32_t c = imul(w[2], ln.m8);   // << 3
+  const uint32_t d = imul(w[3], ln.m32);  // << 5
+  row_valid(w[0], imul(w[0], ln.m8), ln, ag[0], ay[0]);
+  row_valid(w[1], imul(w[1], ln.m8), ln, ag[1], ay[1]);
+  row_valid(w[2], c, ln, ag[2], ay[2]);
+  row_valid(w[3], imul(w[3], ln.m8), ln, ag[3], ay[3]);
+  uint32_t m = (a & 0x03030303u) | (b & ~0x03030303u);
+  m = (m & 0x0F0F0F0Fu) | (c & ~0x0F0F0F0Fu);
+  return (m & 0x3F3F3F3Fu) | (d & ~0x3F3F3F3Fu);
+}
+
+// after transpose3 of a raw merged word: low plane = b1 ^ b2
+__device__ __forceinline__ uint32_t low_fix(uint32_t m, const Lane& ln) {
+  const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, m, 4);
+  return m ^ (y & ln.lofix);
+}
+
 }  // namespace enc3
+
+#ifndef GK_ENC3_RAW
+#define GK_ENC3_RAW 1
+#endif
 
 // ---- group encoder of encode3_kernel (gk_encode.cu): outputs collected per
 // block of 4 groups in shared memory, [plane][position * 5 + group]
@@ -151,10 +193,13 @@ __device__ __forceinline__ void enc3_chunk(const uint8_t* buf, const uint32_t (&
           rem >= 4 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * rem)));
       w = (w & bm) | (0x41414141u & ~bm);
     }
-    x[i] = enc3::row_word(w, ln, ag[i], ay[i]);
+    if (GK_ENC3_RAW) x[i] = w;
+    else x[i] = enc3::row_word(w, ln, ag[i], ay[i]);
   }
-  uint32_t m = enc3::merge4(x[0], x[1], x[2], x[3], ln);
+  uint32_t m = GK_ENC3_RAW ? enc3::merge4_raw(x, ln, ag, ay)
+                           : enc3::merge4(x[0], x[1], x[2], x[3], ln);
   m = enc3::transpose3(m, ln);
+  if (GK_ENC3_RAW) m = enc3::low_fix(m, ln);
   // lane = cw + 4b' + 8k: position 16c + 4cw + k, plane b' (0 = low -> paper plane 1)
   const int lane = threadIdx.x & 31;
   const int pos = 16 * c + 4 * (lane & 3) + (lane >> 3);
@@ -185,14 +230,17 @@ __device__ __forceinline__ uint32_t enc3_merge_m2(const uint8_t* buf, const uint
       bm &= rem >= 4 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * rem)));
     }
     if (first || tail) w = (w & bm) | (0x41414141u & ~bm);
-    x[i] = enc3::row_word(w, ln, ag[i], ay[i]);
+    if (GK_ENC3_RAW) x[i] = w;
+    else x[i] = enc3::row_word(w, ln, ag[i], ay[i]);
   }
+  if (GK_ENC3_RAW) return enc3::merge4_raw(x, ln, ag, ay);
   return enc3::merge4(x[0], x[1], x[2], x[3], ln);
 }
 
 __device__ __forceinline__ void enc3_emit(uint32_t m, int c, int len, const enc3::Lane& ln,
                                           uint32_t* outs, uint32_t P, int wg) {
   m = enc3::transpose3(m, ln);
+  if (GK_ENC3_RAW) m = enc3::low_fix(m, ln);
   const int lane = threadIdx.x & 31;
   const int pos = 16 * c + 4 * (lane & 3) + (lane >> 3);
   const int plane = ((lane >> 2) & 1) ? 0 : 1;
