@@ -648,7 +648,7 @@ def measure_e2e(args, ctx, bk):
     torch, gk, sharding = ctx["torch"], ctx["gk"], ctx["sharding"]
     world, rank, dev = ctx["world"], ctx["rank"], ctx["dev"]
     c5 = args.config == "c5"
-    t_step, h2d, d2h, desc = 0.0, 0, 0, []
+    t_step, t_sample, h2d, d2h, desc = 0.0, 0.0, 0, 0, []
     for L, es, idx0, n in bk:
         lo, cnt = sharding.even_shard(n, rank, world) if c5 else sharding.weak_shard(n, rank)
         # pinned host sample per rank (8M pairs per bucket at N=1, less per rank at N>1
@@ -687,6 +687,7 @@ def measure_e2e(args, ctx, bk):
             one()
         dt = (time.perf_counter() - t0) / reps
         t_step += dt * cnt / ns
+        t_sample += dt
         h2d += 2 * ns * L
         if c5:
             _, _, got = gk.filter_host(hr, hf, es[0], L, want_accept=False, indices=True, idx=idx,
@@ -701,8 +702,26 @@ def measure_e2e(args, ctx, bk):
         torch.cuda.empty_cache()
     t_all = sharding.max_over_ranks(t_step, device=dev)
     work = sum(n * len(es) for _, es, _, n in bk) * (1 if c5 else world)
+    # the PCIe roofline of this number: a plain pinned host->device copy on this box
+    buf_h = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    buf_d = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    buf_d.copy_(buf_h, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        buf_d.copy_(buf_h, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    h2d_peak = 3 * (1 << 30) / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del buf_h, buf_d
+    h2d_rate = h2d / t_sample / 1e9
     return {"value": round(work / t_all / 1e9, 4), "unit": unit_of(args),
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "bytes_note": "h2d/d2h bytes of one timed repetition (the sample below); value is "
+                          "scaled from the sample's time per pair to the whole workload",
+            "h2d_GB_s": round(h2d_rate, 2), "h2d_copy_peak_GB_s": round(h2d_peak, 2),
+            "pcie_frac": round(h2d_rate / h2d_peak, 4),
             "api": ("gk_filter_host (pinned host ASCII; per 2M-pair chunk gk_encode x2 + gk_filter "
                     "+ gk_compact, only the accepted pairs' indices come back; 2 CUDA streams "
                     "overlapping H2D / kernels / D2H)" if c5 else
