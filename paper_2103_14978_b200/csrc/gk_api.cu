@@ -302,18 +302,28 @@ int host_begin(void* stream, HostRes** out) {
   if (dev < 0 || dev >= kMaxDev) return GK_ERR_ARG;
   HostRes& r = g_host[dev];
   if (!r.ready) {
-    for (int b = 0; b < 2; ++b) {
-      if ((err = cudaStreamCreateWithFlags(&r.st[b], cudaStreamNonBlocking)) != cudaSuccess)
-        return cuda_status(err);
-      if ((err = cudaEventCreateWithFlags(&r.ev_cnt[b], cudaEventDisableTiming)) != cudaSuccess)
-        return cuda_status(err);
+    // create everything or nothing: a partial failure releases what was created
+    HostRes t;
+    t.st[0] = t.st[1] = nullptr;
+    t.ev_in = t.ev_cnt[0] = t.ev_cnt[1] = nullptr;
+    for (int b = 0; b < 2 && err == cudaSuccess; ++b) {
+      err = cudaStreamCreateWithFlags(&t.st[b], cudaStreamNonBlocking);
+      if (err == cudaSuccess) err = cudaEventCreateWithFlags(&t.ev_cnt[b], cudaEventDisableTiming);
     }
-    if ((err = cudaEventCreateWithFlags(&r.ev_in, cudaEventDisableTiming)) != cudaSuccess)
+    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&t.ev_in, cudaEventDisableTiming);
+    if (err == cudaSuccess)
+      err = cudaHostAlloc(reinterpret_cast<void**>(&t.cnt), 2 * sizeof(unsigned long long),
+                          cudaHostAllocDefault);
+    if (err != cudaSuccess) {
+      for (int b = 0; b < 2; ++b) {
+        if (t.st[b]) cudaStreamDestroy(t.st[b]);
+        if (t.ev_cnt[b]) cudaEventDestroy(t.ev_cnt[b]);
+      }
+      if (t.ev_in) cudaEventDestroy(t.ev_in);
       return cuda_status(err);
-    if ((err = cudaHostAlloc(reinterpret_cast<void**>(&r.cnt), 2 * sizeof(unsigned long long),
-                             cudaHostAllocDefault)) != cudaSuccess)
-      return cuda_status(err);
-    r.ready = true;
+    }
+    t.ready = true;
+    r = t;
   }
   // order both pipeline streams after the caller's stream (its producers of
   // device inputs / workspace)
