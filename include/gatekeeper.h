@@ -121,7 +121,7 @@ int gk_filter(const uint32_t* d_reads_packed, const uint32_t* d_refs_packed,
  * (:136, :238); it runs on the block-transposed kernel. */
 #define GK_FLAG_GENERIC 1
 #define GK_FLAG_NO_EDGE_FIX 2
-/* GK_FLAG_BLOCKED forces the block-transposed kernel (8-position blocks x all
+/* GK_FLAG_BLOCKED forces the block-transposed kernel (16-position blocks x all
  * masks, any e; the default for e above the all-register instantiations) --
  * diagnostic / test knob: results are identical. */
 #define GK_FLAG_BLOCKED 4

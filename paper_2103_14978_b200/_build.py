@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libgk.so")
 SOURCES = ["gk_api.cu", "gk_encode.cu", "gk_filter.cu", "gk_filter_ascii.cu", "gk_compact.cu",
            "gk_filter_ascii_p0.cu", "gk_filter_ascii_p1.cu", "gk_filter_ascii_p2.cu",
-           "gk_filter_ascii_p3.cu", "gk_filter_bt.cu", "gk_filter_bt2.cu", "gk_fused.cu", "gk_verify.cu", "gk_index.cu"]
+           "gk_filter_ascii_p3.cu", "gk_filter_bt2.cu", "gk_fused.cu", "gk_verify.cu", "gk_index.cu"]
 HEADERS = ["gk_common.cuh", "gk_kernels.cuh", "gk_encode_core.cuh", "gk_filter_core.cuh",
            "gk_tma.cuh", "gk_filter_ascii_impl.cuh", "gk_encode3.cuh", "gk_bt2.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -33,7 +33,7 @@ def stale() -> bool:
 
 def build(verbose: bool = False, force: bool = False, jobs: int | None = None,
           defines=(), out: str | None = None) -> str:
-    """Build libgk.so (or, with `defines` such as ["GK_BT2=0"], an A/B variant at `out`)."""
+    """Build libgk.so (or, with `defines` such as ["GK_BT2_B=16"], an A/B variant at `out`)."""
     so = out or SO
     if not force and not defines and not stale():
         return SO

@@ -121,18 +121,9 @@ static bool dispatch_sp(int e, const uint2* reads, const uint2* refs, const uint
   return false;
 }
 
-void launch_bt(const uint2* reads, const uint2* refs, const uint32_t* rund, const uint32_t* fund,
-               int64_t n, int len, int e, uint32_t* accept, uint8_t* errc, int edge_fix,
-               cudaStream_t stream);
 void launch_bt2(const uint2* reads, const uint2* refs, const uint32_t* rund, const uint32_t* fund,
                 int64_t n, int len, int e, uint32_t* accept, uint8_t* errc, int edge_fix,
                 cudaStream_t stream);
-// GK_BT2=1 (default): the rolled block-transposed kernels of gk_filter_bt2.cu; 0: the
-// round-1 unrolled-ring kernels of gk_filter_bt.cu (A/B knob)
-#ifndef GK_BT2
-#define GK_BT2 1
-#endif
-
 int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* rund,
                   const uint32_t* fund, int64_t n, int len, int e, uint32_t* accept,
                   uint8_t* errc, int flags, cudaStream_t stream) {
@@ -145,8 +136,7 @@ int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* r
   // measured 1.3-1.7x faster than the earlier warp-pair split at e = 12..25
   // (profiles/r01_cmp_bt.jsonl)
   if (!force_generic && ((flags & 4) || !edge_fix || e > GK_SP_EMAX)) {
-    if (GK_BT2) launch_bt2(r2, f2, rund, fund, n, len, e, accept, errc, edge_fix, stream);
-    else launch_bt(r2, f2, rund, fund, n, len, e, accept, errc, edge_fix, stream);
+    launch_bt2(r2, f2, rund, fund, n, len, e, accept, errc, edge_fix, stream);
     return 0;
   }
   if (!force_generic &&
@@ -168,9 +158,6 @@ int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* r
   return 0;
 }
 
-void launch_bt_sweep(const uint2* reads, const uint2* refs, const uint32_t* rund,
-                     const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,
-                     uint8_t* errc, int edge_fix, cudaStream_t stream);
 void launch_bt2_sweep(const uint2* reads, const uint2* refs, const uint32_t* rund,
                       const uint32_t* fund, int64_t n, int len, int emax, uint32_t* accept,
                       uint8_t* errc, int edge_fix, cudaStream_t stream);
@@ -189,7 +176,7 @@ int launch_filter_sweep(const uint32_t* reads, const uint32_t* refs, const uint3
   const int np = maxc < 64 ? 6 : (maxc < 128 ? 7 : 8);
   const size_t smem = (size_t)2 * emax * np * 32 * 4;
   if (smem <= 200 * 1024) {
-    (GK_BT2 ? launch_bt2_sweep : launch_bt_sweep)(
+    launch_bt2_sweep(
         reinterpret_cast<const uint2*>(reads), reinterpret_cast<const uint2*>(refs), rund, fund, n,
         len, emax, accept, errc, (flags & 2) ? 0 : 1, stream);
     return 0;

@@ -2,7 +2,7 @@
 // k loop: the kernels behind gk_filter for e above the all-register single pass
 // and behind gk_filter_sweep (every e <= e_max in one pass).
 //
-// Loop order (as gk_filter_bt.cu): per block of B positions [ib, ib+B) of a
+// Loop order: per block of B positions [ib, ib+B) of a
 // tile, the Hamming mask, then for k = 1..e the deletion and insertion masks of
 // the block (W = B+4 cells: the block plus the 2-base amendment halo on each
 // side), ANDed into the block's B words of F:
@@ -10,7 +10,7 @@
 //   H   x[c] = R[j] != Q[j]          D_k  x[c] = R[j] != Q[j-k]
 //   I_k x[c] = R[j] != Q[j+k]        (j = ib-2+c; Q = read, R = reference)
 //
-// What differs from gk_filter_bt.cu (round 1, 13-step unrolled register ring +
+// What differs from round 1's gk_filter_bt.cu (removed in round 2; 13-step unrolled register ring +
 // an out-of-line per-k counter): the two read windows slide by plain register
 // moves inside a ROLLED k loop -- the moves issue on the FMA pipe (IMAD.MOV)
 // while the ALU pipe (LOP3) is the bottleneck, so they are nearly free, and the
@@ -21,7 +21,7 @@
 //
 // Blocks whose steps would touch a vacated source, a vacated position or a
 // target outside [0, len) run those steps CHECKED (rolled, validity words per
-// cell, readings R2 / R4 / R13), exactly as gk_filter_bt.cu.
+// cell, readings R2 / R4 / R13).
 #include "gk_bt2.cuh"
 #include "gk_common.cuh"
 #include "gk_filter_core.cuh"
