@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libgk.so")
 SOURCES = ["gk_api.cu", "gk_encode.cu", "gk_filter.cu", "gk_filter_ascii.cu", "gk_compact.cu",
            "gk_filter_ascii_p0.cu", "gk_filter_ascii_p1.cu", "gk_filter_ascii_p2.cu",
-           "gk_filter_ascii_p3.cu", "gk_filter_bt2.cu", "gk_fused.cu", "gk_verify.cu", "gk_index.cu"]
+           "gk_filter_ascii_p3.cu", "gk_filter_bt2.cu", "gk_filter_sp2.cu", "gk_fused.cu", "gk_verify.cu", "gk_index.cu"]
 HEADERS = ["gk_common.cuh", "gk_kernels.cuh", "gk_encode_core.cuh", "gk_filter_core.cuh",
            "gk_tma.cuh", "gk_filter_ascii_impl.cuh", "gk_encode3.cuh", "gk_bt2.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

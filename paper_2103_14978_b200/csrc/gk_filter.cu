@@ -121,6 +121,11 @@ static bool dispatch_sp(int e, const uint2* reads, const uint2* refs, const uint
   return false;
 }
 
+#ifndef GK_SP2
+#define GK_SP2 1
+#endif
+bool launch_sp2(const uint2* reads, const uint2* refs, const uint32_t* rund, const uint32_t* fund,
+                int64_t n, int len, int e, uint32_t* accept, uint8_t* errc, cudaStream_t stream);
 void launch_bt2(const uint2* reads, const uint2* refs, const uint32_t* rund, const uint32_t* fund,
                 int64_t n, int len, int e, uint32_t* accept, uint8_t* errc, int edge_fix,
                 cudaStream_t stream);
@@ -136,6 +141,11 @@ int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* r
   // measured 1.3-1.7x faster than the earlier warp-pair split at e = 12..25
   // (profiles/r01_cmp_bt.jsonl)
   if (!force_generic && ((flags & 4) || !edge_fix || e > GK_SP_EMAX)) {
+    // e just above the all-register single pass: the warp-pair split single pass
+    // (gk_filter_sp2.cu), else the block-transposed kernel (any e, any flags)
+    if (GK_SP2 && !(flags & 4) && edge_fix &&
+        launch_sp2(r2, f2, rund, fund, n, len, e, accept, errc, stream))
+      return 0;
     launch_bt2(r2, f2, rund, fund, n, len, e, accept, errc, edge_fix, stream);
     return 0;
   }

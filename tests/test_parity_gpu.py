@@ -153,6 +153,20 @@ def test_adversarial_sets(gk):
             assert_parity(gk, reads, refs, e, path="packed", flags=gk.GK_FLAG_BLOCKED)
 
 
+@pytest.mark.parametrize("L", [13, 14, 15, 16, 20, 24, 25, 33, 100, 150, 250, 251, 508])
+def test_split_single_pass_e12(gk, L):
+    """e = 12 runs the warp-pair split single pass (gk_filter_sp2.cu): every length
+    class of its checked / unchecked batches (len < 8 + E, ragged last batch), ragged
+    tile counts, undefined / lower-case / IUPAC bytes (balanced profile) and the paper
+    profile; == the oracle and == the block-transposed kernel (GK_FLAG_BLOCKED)."""
+    e = 12
+    for n, prof, seed in ((3000, pairgen.PROFILE_BALANCED, L), (2049, pairgen.PROFILE_PAPER, L + 1),
+                          (33, pairgen.PROFILE_BALANCED, L + 2)):
+        reads, refs = pairgen.gen_pairs(n, L, profile=prof, emax=e, seed=seed)
+        assert_parity(gk, reads, refs, e, path="packed")
+        assert_parity(gk, reads, refs, e, path="packed", flags=gk.GK_FLAG_BLOCKED)
+
+
 def test_ragged_counts(gk):
     L = 100
     for n in (1, 31, 32, 33, 1023, 1024, 1025, 4097):
