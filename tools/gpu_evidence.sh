@@ -18,7 +18,7 @@ done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c5.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/launches_c5.log 2>&1; echo "launches rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c2.csv python bench.py --config c2 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/launches_c2.log 2>&1; echo "launches c2 rc=$?"
 KEEP="encode3_c5 filter_bt2_sweep_c4"
-for spec in "encode3@c5" "filter_sp@c5" "filter_bt2_kernel@c5" "compact_write@c5" "filter_bt2_sweep@c2" "filter_bt2_sweep@c3" "filter_bt2_sweep@c4" "encode3@c2" "encode3@c4"; do
+for spec in "encode3@c5" "filter_sp@c5" "filter_sp2@c5" "compact_write@c5" "filter_bt2_sweep@c2" "filter_bt2_sweep@c3" "filter_bt2_sweep@c4" "encode3@c2" "encode3@c4"; do
   k=${spec%%@*}; cfg=${spec#*@}; name=ncu_${k}_$cfg
   timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$k" -c 1 -o $OUT/$name python bench.py --config $cfg --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $OUT/$name.log 2>&1; echo "ncu $k $cfg rc=$?"
   python tools/ncu_summary.py $OUT/$name.ncu-rep > $OUT/$name.summary.txt 2>&1
