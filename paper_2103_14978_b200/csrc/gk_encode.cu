@@ -29,6 +29,9 @@
 #ifndef GK_ENC3_PF
 #define GK_ENC3_PF 0  // L2 prefetch distance in blocks (A/B knob; 1-2 measured 1.1-1.5x slower)
 #endif
+#ifndef GK_ENC3_VEC
+#define GK_ENC3_VEC 1  // copy-out with 16-byte stores (below 241 bp)
+#endif
 #ifndef GK_ENCODE_TMA
 #define GK_ENCODE_TMA 1
 #endif
@@ -165,11 +168,22 @@ __global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restr
     // write the 4 groups' words: per position 32 contiguous bytes
     const int64_t tile = (4 * b) >> 5;
     const int gl0 = (int)((4 * b) & 31);
-    uint2* dst = reinterpret_cast<uint2*>(packed);
-    for (int t = threadIdx.x; t < 4 * len; t += 128) {
-      const int pos = t >> 2, w = t & 3;
-      dst[((tile * len + pos) * 32 + gl0 + w)] =
-          make_uint2(outs[pos * 5 + w], outs[P + pos * 5 + w]);
+    // 16-byte stores (two groups, both planes, per thread and step): +2-3% at 100 / 150
+    // bp, -1.4% at 250 bp (profiles/r02_ab_encoder_vec.jsonl), so not at 250 bp
+    if (GK_ENC3_VEC && NCH != 16) {
+      uint4* dst4 = reinterpret_cast<uint4*>(packed) + ((tile * len) * 32 + gl0) / 2;
+      for (int t = threadIdx.x; t < 2 * len; t += 128) {
+        const int pos = t >> 1, w = (t & 1) * 2;
+        const uint32_t* o = outs + pos * 5 + w;
+        dst4[pos * 16 + (w >> 1)] = make_uint4(o[0], o[P], o[1], o[P + 1]);
+      }
+    } else {
+      uint2* dst = reinterpret_cast<uint2*>(packed);
+      for (int t = threadIdx.x; t < 4 * len; t += 128) {
+        const int pos = t >> 2, w = t & 3;
+        dst[((tile * len + pos) * 32 + gl0 + w)] =
+            make_uint2(outs[pos * 5 + w], outs[P + pos * 5 + w]);
+      }
     }
   }
 }
