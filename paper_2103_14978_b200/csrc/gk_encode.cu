@@ -29,6 +29,9 @@
 #ifndef GK_ENC3_PF
 #define GK_ENC3_PF 0  // L2 prefetch distance in blocks (A/B knob; 1-2 measured 1.1-1.5x slower)
 #endif
+#ifndef GK_ENC3_OB
+#define GK_ENC3_OB 0  // output staging buffers (0: per length class)
+#endif
 #ifndef GK_ENC3_VEC
 #define GK_ENC3_VEC 1  // copy-out with 16-byte stores (below 241 bp)
 #endif
@@ -96,7 +99,7 @@ __global__ void encode_tail_kernel(int64_t first_group, int64_t end_group, int l
 // 8 bytes per position).
 // NCH > 0: compile-time number of 16-position chunks (immediate LDS offsets);
 // NCH == 0: runtime.  ALN: every row start is 4-byte aligned (stride % 4 == 0).
-template <int NCH, int MODE, int MB, int NB>
+template <int NCH, int MODE, int MB, int NB, int OB>
 __global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restrict__ seqs,
                                                          int64_t nblocks, int len, int stride,
                                                          uint32_t bufb, uint32_t P,
@@ -105,8 +108,8 @@ __global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restr
   extern __shared__ __align__(128) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* stage = sm + (size_t)warp * NB * bufb;                              // [NB][bufb]
-  uint32_t* outs = reinterpret_cast<uint32_t*>(sm + (size_t)4 * NB * bufb);    // [2][P]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(outs + 2 * P);
+  uint32_t* outs0 = reinterpret_cast<uint32_t*>(sm + (size_t)4 * NB * bufb);   // [OB][2][P]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(outs0 + OB * 2 * P);
   uint64_t* mybar = bars + 2 * warp;
   if (lane == 0) {
     mbar_init(&mybar[0], 1);
@@ -151,9 +154,12 @@ __global__ void __launch_bounds__(128, MB) encode3_kernel(const uint8_t* __restr
     }
     mbar_wait(&mybar[buf], NB == 2 ? ((uint32_t)(it >> 1) & 1u) : ((uint32_t)it & 1u));
     const uint8_t* sbuf = stage + buf * bufb;
-    // one output staging buffer (smem for more CTAs per SM): the previous block's
-    // copy-out must be complete before it is overwritten
-    if (it > 0) __syncthreads();
+    // OB = 1 output staging buffer (smem for more CTAs per SM): the previous block's
+    // copy-out must be complete before it is overwritten; OB = 2: the barrier before
+    // the copy-out of block it+1 already orders the copy-out of block it before the
+    // encode of block it+2 into the same buffer
+    uint32_t* outs = outs0 + (OB == 2 ? (size_t)(it & 1) * 2 * P : 0);
+    if (OB == 1 && it > 0) __syncthreads();
     const uint32_t und = enc3_group<NCH, MODE>(sbuf, roff, rsh, s2, len, ln, outs, P, warp);
     if (lane == 0) undef[4 * b + warp] = und;
     if (NB == 1) {  // single buffer: the next span lands during the copy-out below
@@ -193,13 +199,13 @@ struct Enc3Cfg {
   size_t smem;
 };
 
-static Enc3Cfg enc3_cfg(int len, int stride, int nbuf) {
+static Enc3Cfg enc3_cfg(int len, int stride, int nbuf, int nob) {
   Enc3Cfg c;
   c.bufb = ((uint32_t)(32 * stride + 32) + 127u) & ~127u;
   uint32_t p = (uint32_t)(5 * len);
   p = (p + 31u) & ~31u;
   c.P = p + 16u;  // P = 16 (mod 32): the two planes' transposed writes hit disjoint banks
-  c.smem = (size_t)4 * nbuf * c.bufb + (size_t)2 * c.P * 4 + 8 * 8;
+  c.smem = (size_t)4 * nbuf * c.bufb + (size_t)nob * 2 * c.P * 4 + 8 * 8;
   return c;
 }
 
@@ -212,8 +218,11 @@ static void launch_enc3_t(const uint8_t* seqs, int64_t nblocks, int len, int str
   // buffered at 7 (2.40 -> 2.25 ms); 250 bp single-buffered at 5 (3.95 -> 3.51 ms)
   constexpr int MB = GK_ENC3_MINB > 0 ? GK_ENC3_MINB : (NCH == 7 ? 8 : (NCH == 10 ? 7 : (NCH == 16 ? 5 : 1)));
   constexpr int NB = GK_ENC3_NBUF > 0 ? GK_ENC3_NBUF : (NCH == 7 || NCH == 0 ? 2 : 1);
-  const Enc3Cfg c = enc3_cfg(len, stride, NB);
-  auto kern = encode3_kernel<NCH, MODE, MB, NB>;
+  // 150 bp: a second output staging buffer still fits 7 CTAs/SM and saves one CTA
+  // barrier per block (profiles/r02_ab_encoder_ob.jsonl)
+  constexpr int OB = GK_ENC3_OB > 0 ? GK_ENC3_OB : (NCH == 10 ? 2 : 1);
+  const Enc3Cfg c = enc3_cfg(len, stride, NB, OB);
+  auto kern = encode3_kernel<NCH, MODE, MB, NB, OB>;
   // launch configuration cached per (device, smem): the attribute and occupancy
   // queries are host round trips, kept off the per-call path
   static thread_local int cached_dev = -1, cached_grid = 0;
