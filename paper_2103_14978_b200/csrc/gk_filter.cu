@@ -16,6 +16,15 @@
 #include "gk_filter_core.cuh"
 #include "gk_kernels.cuh"
 
+// resident CTAs per SM asked of ptxas for sp<6>, sp<7> (3: 168 registers instead of
+// 172-186, 12 warps instead of 8; 150 bp e=7 0.82 -> 0.78 ms, 100 bp e=6 0.51 -> 0.47 ms
+// per 30M pairs, profiles/r02_ab_sp_minb.jsonl) and sp<4>, sp<5> (A/B knob)
+#ifndef GK_SP_MINB67
+#define GK_SP_MINB67 3
+#endif
+#ifndef GK_SP_MINB45
+#define GK_SP_MINB45 1
+#endif
 #ifndef GK_FILTER_RING
 #define GK_FILTER_RING 1
 #endif
@@ -23,7 +32,7 @@
 namespace gk {
 
 template <int E>
-__global__ void __launch_bounds__(128) filter_sp_kernel(
+__global__ void __launch_bounds__(128, (E >= 6 && E <= 7) ? GK_SP_MINB67 : ((E >= 4 && E <= 5) ? GK_SP_MINB45 : 1)) filter_sp_kernel(
     const uint2* __restrict__ reads, const uint2* __restrict__ refs,
     const uint32_t* __restrict__ rund, const uint32_t* __restrict__ fund, int64_t n, int len,
     uint32_t* __restrict__ accept, uint8_t* __restrict__ errc) {
