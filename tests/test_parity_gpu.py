@@ -131,8 +131,10 @@ def test_random_lengths(gk, L):
         assert_parity(gk, reads, refs, e, path="packed", flags=gk.GK_FLAG_BLOCKED)
 
 
-def test_adversarial_sets(gk):
-    L = 48
+@pytest.mark.parametrize("L", [48, 160])
+def test_adversarial_sets(gk, L):
+    """Structured inputs at a short length and at one that takes the split single
+    pass for e = 12 (L >= 128)."""
     rng = np.random.default_rng(1)
     base = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, (512, L))]
     sets = []
@@ -147,7 +149,7 @@ def test_adversarial_sets(gk):
     q = base.copy(); q[::7, 10] = ord("N"); sets.append((q, base.copy()))        # undefined
     q = base.copy() | 0x20; sets.append((q, base.copy()))                        # lower case
     for reads, refs in sets:
-        for e in (0, 1, 2, 4, 8, 15, 23, 47):
+        for e in (0, 1, 2, 4, 8, 12, 15, 23, 47):
             assert_parity(gk, reads, refs, e, path="packed")
             assert_parity(gk, reads, refs, e, path="ascii")
             assert_parity(gk, reads, refs, e, path="packed", flags=gk.GK_FLAG_BLOCKED)
