@@ -21,6 +21,33 @@ int launch_gather_windows(const uint32_t* planes, int64_t nbases, const int64_t*
 }  // namespace gk
 
 static thread_local int g_last_cuda_error = 0;
+
+namespace gk {
+void ensure_func_attr(const void* f, cudaFuncAttribute attr, int value) {
+  struct Entry {
+    int dev;
+    const void* f;
+    int attr;
+    int value;
+  };
+  static thread_local Entry seen[256];
+  static thread_local int nseen = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (int i = 0; i < nseen; ++i) {
+    Entry& e = seen[i];
+    if (e.dev == dev && e.f == f && e.attr == (int)attr) {
+      if (e.value != value) {
+        cudaFuncSetAttribute(f, attr, value);
+        e.value = value;
+      }
+      return;
+    }
+  }
+  cudaFuncSetAttribute(f, attr, value);
+  if (nseen < 256) seen[nseen++] = Entry{dev, f, (int)attr, value};
+}
+}  // namespace gk
 static std::atomic<uint64_t> g_launches{0};
 
 namespace gk {

@@ -280,10 +280,10 @@ static void launch_generic(const uint8_t* seqs, int64_t n, int len, int64_t stri
   const int64_t blocks = (ngroups + gpc - 1) / gpc;
   const bool aligned = (stride % 4 == 0) && ((reinterpret_cast<uintptr_t>(seqs) & 3u) == 0);
   if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    ensure_func_attr((const void*)encode_kernel<true>,
+                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_func_attr((const void*)encode_kernel<false>,
+                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   count_launch();
   if (aligned)

@@ -111,8 +111,8 @@ static void launch_sp(const uint2* reads, const uint2* refs, const uint32_t* run
   const int64_t blocks = (tiles + warps - 1) / warps;
   const size_t smem = GK_FILTER_RING ? (size_t)warps * (2 * 4 * 8 * 32 * 8 + 64) : 0;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(filter_sp_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    ensure_func_attr((const void*)filter_sp_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                     (int)smem);
   count_launch();
   filter_sp_kernel<E><<<(unsigned)blocks, warps * 32, smem, stream>>>(reads, refs, rund, fund, n,
                                                                        len, accept, errc);
@@ -167,8 +167,8 @@ int launch_filter(const uint32_t* reads, const uint32_t* refs, const uint32_t* r
   if (warps < 1) warps = 1;
   const size_t smem = (size_t)warps * len * 32 * 4;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(filter_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    ensure_func_attr((const void*)filter_generic_kernel,
+                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t blocks = (tiles + warps - 1) / warps;
   count_launch();
   filter_generic_kernel<<<(unsigned)blocks, warps * 32, smem, stream>>>(r2, f2, rund, fund, n,

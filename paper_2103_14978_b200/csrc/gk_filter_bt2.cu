@@ -129,11 +129,8 @@ void launch_bt2(const uint2* reads, const uint2* refs, const uint32_t* rund, con
   const int64_t tiles = (n + 1023) / 1024;
   const int warps = GK_BT2_E_WARPS;
   const int64_t blocks = (tiles + warps - 1) / warps;
-  static thread_local bool attr_set = false;  // L1 carveout: once per thread
-  if (!attr_set) {
-    cudaFuncSetAttribute(filter_bt2_kernel<B>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-    attr_set = true;
-  }
+  ensure_func_attr((const void*)filter_bt2_kernel<B>,
+                   cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // all L1
   count_launch();
   filter_bt2_kernel<B><<<(unsigned)blocks, warps * 32, 0, stream>>>(reads, refs, rund, fund, n,
                                                                     len, e, accept, errc, edge_fix);
@@ -147,12 +144,9 @@ static void launch_bt2_sweep_np(const uint2* reads, const uint2* refs, const uin
   const int64_t tiles = (n + 1023) / 1024;
   const int64_t blocks = (tiles + BT2_SWEEP_WARPS - 1) / BT2_SWEEP_WARPS;
   const size_t smem = (size_t)BT2_SWEEP_WARPS * emax * NP * 32 * 4;
-  static thread_local size_t attr_smem = 0;
-  if (smem > 48 * 1024 && smem > attr_smem) {
-    cudaFuncSetAttribute(filter_bt2_sweep_kernel<B, NP, MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_smem = smem;
-  }
+  if (smem > 48 * 1024)
+    ensure_func_attr((const void*)filter_bt2_sweep_kernel<B, NP, MINB>,
+                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   count_launch();
   filter_bt2_sweep_kernel<B, NP, MINB><<<(unsigned)blocks, BT2_SWEEP_WARPS * 32, smem, stream>>>(
       reads, refs, rund, fund, n, len, emax, accept, errc, edge_fix);

@@ -286,12 +286,8 @@ static void launch_sp2_t(const uint2* reads, const uint2* refs, const uint32_t* 
                          uint8_t* errc, cudaStream_t stream) {
   const int64_t tiles = (n + 1023) / 1024;
   const int64_t blocks = (tiles + 1) / 2;
-  static thread_local bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(filter_sp2_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sp2::kSmem);
-    attr = true;
-  }
+  ensure_func_attr((const void*)filter_sp2_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                   (int)sp2::kSmem);
   count_launch();
   filter_sp2_kernel<E><<<(unsigned)blocks, 128, sp2::kSmem, stream>>>(reads, refs, rund, fund, n,
                                                                        len, accept, errc);

@@ -422,22 +422,10 @@ template <class K>
 static void launch(K kern, const Layout& L, int64_t n, const uint8_t* reads, const uint8_t* refs,
                    int stride, int len, int e, uint32_t* accept, uint8_t* errc,
                    cudaStream_t stream) {
-  // dynamic shared memory opt-in, cached per kernel (all instantiations share K)
-  struct Seen {
-    const void* f;
-    size_t bytes;
-  };
-  static thread_local Seen seen[64];
-  static thread_local int nseen = 0;
-  if (L.total > 48 * 1024) {
-    int i = 0;
-    while (i < nseen && seen[i].f != (const void*)kern) ++i;
-    if (i == nseen || seen[i].bytes < L.total) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-      if (i == nseen && nseen < 64) ++nseen;
-      if (i < 64) seen[i] = Seen{(const void*)kern, L.total};
-    }
-  }
+  // dynamic shared memory opt-in (per device and kernel)
+  if (L.total > 48 * 1024)
+    ensure_func_attr((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                     (int)L.total);
   const int64_t tiles = (n + 1023) / 1024;
   count_launch();
   kern<<<(unsigned)tiles, NW * 32, L.total, stream>>>(reads, refs, stride, n, len, e, L, accept,

@@ -13,6 +13,11 @@ namespace gk {
 // C ABI): the bench's "gpu_launches" is read from it, not estimated.
 void count_launch(int k = 1);
 
+// cudaFuncSetAttribute(f, attr, value) on the current device unless this host
+// thread already set that value there (attributes are per device: a thread that
+// drives several GPUs sets them on each; repeated calls stay off the host path).
+void ensure_func_attr(const void* f, cudaFuncAttribute attr, int value);
+
 int launch_encode(const uint8_t* seqs, int64_t n, int len, int64_t stride, uint32_t* packed,
                   uint32_t* undef, cudaStream_t stream);
 

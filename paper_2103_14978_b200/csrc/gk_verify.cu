@@ -107,8 +107,8 @@ static void launch_ed(const uint8_t* reads, const uint8_t* refs, int64_t stride,
                       int len, int32_t* dist, cudaStream_t stream) {
   const size_t smem = (size_t)8 * W * ED_THREADS * 8;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(edit_distance_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    ensure_func_attr((const void*)edit_distance_kernel<W>,
+                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t blocks = (n + ED_THREADS - 1) / ED_THREADS;
   count_launch();
   edit_distance_kernel<W><<<(unsigned)blocks, ED_THREADS, smem, stream>>>(reads, refs, stride, n,
