@@ -29,6 +29,9 @@
 #ifndef GK_SP2_MINB
 #define GK_SP2_MINB 3
 #endif
+#ifndef GK_SP2_RING
+#define GK_SP2_RING 1  // 1: per-warp TMA rings; 0: read-only loads + L1 prefetch (A/B knob)
+#endif
 #ifndef GK_SP2_MINLEN
 #define GK_SP2_MINLEN 128  // shorter reads: mostly checked batches, bt2 is faster there
 #endif
@@ -171,6 +174,7 @@ __global__ void __launch_bounds__(128, GK_SP2_MINB) filter_sp2_kernel(
   auto empty_id = [&](int s) { return 2 + pair * 4 + s * 2; };
   const int fin_id = 9 + pair;
   uint8_t* mine = sm_sp2 + (size_t)warp * sp2::kRingBytes;
+#if GK_SP2_RING
   RingSrc src;
   src.gq = reads + tile * (int64_t)len * 32;
   src.gr = refs + tile * (int64_t)len * 32;
@@ -191,6 +195,13 @@ __global__ void __launch_bounds__(128, GK_SP2_MINB) filter_sp2_kernel(
   }
   __syncwarp();
   src.start();
+#else
+  (void)mine;
+  GlobalGroupSrc src;
+  src.q = reads + tile * (int64_t)len * 32 + lane;
+  src.r = refs + tile * (int64_t)len * 32 + lane;
+  src.len = len;
+#endif
   CsaCounter cnt;  // side A: A0 run starts (c0); side B: F run starts
   cnt.clear();
   uint32_t prev = 0u;
@@ -210,6 +221,18 @@ __global__ void __launch_bounds__(128, GK_SP2_MINB) filter_sp2_kernel(
       // checked batches: SIDE A near the start (deletion vacancies, i < E) and at
       // the end (targets >= len); SIDE B near the end (insertion vacancies)
       const bool chk = SIDE == 0 ? (i0 < E || i0 + 8 + 2 > len) : (i0 + 8 + 2 + E > len);
+#if !GK_SP2_RING
+      {  // pull the next batch's words into L1 while this one computes
+        const int pn = i0 + 8 + 2;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (pn + u + H::QNEW < len)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(src.q + (int64_t)(pn + u + H::QNEW) * GK_WARP));
+          if (pn + u < len)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(src.r + (int64_t)(pn + u) * GK_WARP));
+        }
+      }
+#endif
       if (chk) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
