@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(128, GK_SP2_MINB) filter_sp2_kernel(
           const int i = i0 + u;
           h.template step<true, true>(i, len, src.ldq(i + 2 + H::QNEW), src.ldr(i + 2), fp[u],
                                       a0[u]);
+          if (i >= len) fp[u] = a0[u] = 0u;  // positions >= len: never counted (R13)
         }
       } else {
         uint2 qn[8], rn[8];
@@ -269,9 +270,10 @@ __global__ void __launch_bounds__(128, GK_SP2_MINB) filter_sp2_kernel(
       uint32_t st[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const uint32_t f = (i0 + u < len) ? v[u] : 0u;  // positions >= len: never counted (R13)
-        st[u] = f & ~(prev & notstart_of(u));
-        prev = f;
+        // (positions >= len occur only in checked batches, zeroed there: side B's
+        // v = its part & side A's zeroed part)
+        st[u] = v[u] & ~(prev & notstart_of(u));
+        prev = v[u];
       }
       cnt.add8(st);
     }
